@@ -1,0 +1,165 @@
+"""Row-wise α-entmax in float64 — TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+Every function follows PAPER.md (/root/reference/PAPER.md, cited as P:L<n>) in
+the paper's order and notation.  Inputs ``z`` are rows of *pre-scaled* scores
+z = (α−1)·s (Alg. 1 line 3).  Entries equal to −inf are "not visible"
+(causal mask / padding) and contribute nothing; ``n`` in Alg. 1 line 5 is the
+count of visible entries per row (reading c8).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def relu_pow(x: np.ndarray, p: float) -> np.ndarray:
+    """[x]_+^p with the strict-indicator convention [x]_+^p := 0 for x <= 0 for
+    every p (reading c7; Eqs. 6-7 P:L226-227 raise [·]_+ to powers that
+    may be 0 or negative)."""
+    out = np.zeros_like(x, dtype=np.float64)
+    m = x > 0
+    out[m] = np.power(x[m], p)
+    return out
+
+
+def root_f(z: np.ndarray, tau: np.ndarray, alpha: float):
+    """f(τ), f'(τ), f''(τ) of Eq. 3 and Eqs. 6-7, on
+    pre-scaled rows z (shape (..., n)) and per-row τ (shape (...))."""
+    e = 1.0 / (alpha - 1.0)
+    x = z - tau[..., None]
+    f = relu_pow(x, e).sum(-1) - 1.0                                   # Eq. 3
+    f1 = -(1.0 / (alpha - 1.0)) * relu_pow(x, e - 1.0).sum(-1)         # Eq. 6
+    f2 = ((2.0 - alpha) / (alpha - 1.0) ** 2) * relu_pow(x, e - 2.0).sum(-1)  # Eq. 7
+    return f, f1, f2
+
+
+def bracket_init(z: np.ndarray, alpha: float):
+    """Alg. 1 lines 4-6: τ_lo = max − 1, τ_hi = max − n^{1−α},
+    τ = midpoint; n = visible entries per row."""
+    m = z.max(-1)
+    n = np.isfinite(z).sum(-1).astype(np.float64)
+    tau_lo = m - 1.0
+    tau_hi = m - n ** (1.0 - alpha)
+    return tau_lo, tau_hi, 0.5 * (tau_lo + tau_hi)
+
+
+def bisection_update(f, tau, tau_lo, tau_hi):
+    """Eq. 4: (τ_lo, τ) if f(τ) < 0 else (τ, τ_hi).  A tie f = 0
+    takes the 'otherwise' branch (reading c5)."""
+    neg = f < 0
+    return np.where(neg, tau_lo, tau), np.where(neg, tau, tau_hi)
+
+
+def halley_update(f, f1, f2, tau):
+    """Eq. 5: H_f(τ) = τ − 2 f f' / (2 f'^2 − f f'').  Returns
+    (τ_H, ok) with ok False where the denominator is 0 or non-finite (reading c6)."""
+    den = 2.0 * f1 * f1 - f * f2
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tau_h = tau - 2.0 * f * f1 / den
+    ok = np.isfinite(tau_h) & (den != 0)
+    return tau_h, ok
+
+
+def halley_bisection(z: np.ndarray, alpha: float, T: int, return_state: bool = False,
+                     halley: bool = True):
+    """Alg. 1 run for exactly T iterations, row-wise (the "T-step
+    mirror" the GPU is compared against).  Each iteration: evaluate f, f', f'' at
+    the current τ; bracket update (line 8); Halley candidate (line 9); accept it iff
+    inside the *updated* bracket [τ_lo, τ_hi] (inclusive, line 10), else take the
+    midpoint (line 13).  The returned τ is the one after the T-th update (reading
+    c4).  ``halley=False`` gives the pure-bisection scheme of Eq. 4 whose answer is
+    the midpoint after the last bracket update."""
+    if T < 1:
+        raise ValueError("T >= 1 required (S:L54)")
+    z = np.asarray(z, dtype=np.float64)
+    tau_lo, tau_hi, tau = bracket_init(z, alpha)
+    history = []
+    for _ in range(T):
+        f, f1, f2 = root_f(z, tau, alpha)
+        tau_lo, tau_hi = bisection_update(f, tau, tau_lo, tau_hi)
+        mid = 0.5 * (tau_lo + tau_hi)
+        if halley:
+            tau_h, ok = halley_update(f, f1, f2, tau)
+            ok &= (tau_h >= tau_lo) & (tau_h <= tau_hi)
+            tau = np.where(ok, tau_h, mid)
+        else:
+            tau = mid
+        if return_state:
+            history.append((tau.copy(), tau_lo.copy(), tau_hi.copy()))
+    if return_state:
+        return tau, tau_lo, tau_hi, history
+    return tau
+
+
+# ---------------------------------------------------------------------------
+# Exact thresholds (the definition the iteration converges to)
+# ---------------------------------------------------------------------------
+
+def tau_sparsemax(z: np.ndarray) -> np.ndarray:
+    """Exact τ for α = 2 (Euclidean projection onto the simplex),
+    sort-and-scan: k* = max{k : 1 + k z_(k) > Σ_{r<=k} z_(r)},
+    τ = (Σ_{r<=k*} z_(r) − 1)/k*.  Rows of pre-scaled z (α−1 = 1)."""
+    z = np.asarray(z, dtype=np.float64)
+    zs = -np.sort(-z, axis=-1)
+    zs_f = np.where(np.isfinite(zs), zs, 0.0)
+    cs = np.cumsum(zs_f, axis=-1)
+    k = np.arange(1, z.shape[-1] + 1, dtype=np.float64)
+    cond = (1.0 + k * zs_f > cs) & np.isfinite(zs)
+    kstar = cond.shape[-1] - np.argmax(cond[..., ::-1], axis=-1)   # last True (1-based)
+    csk = np.take_along_axis(cs, (kstar - 1)[..., None], -1)[..., 0]
+    return (csk - 1.0) / kstar
+
+
+def tau_entmax15(z: np.ndarray) -> np.ndarray:
+    """Exact τ for α = 1.5 by the sort-based method of Peters et al.,
+    derived from Eq. 3 with exponent 1/(α−1) = 2 on a fixed top-k support:
+    Σ_{r<=k} (z_(r) − τ)^2 = 1  ⇒  τ_k = μ_k − sqrt((1 − k·σ²_k)/k)
+    (μ_k mean, σ²_k = mean of squares − μ_k² of the top k), and
+    k* = max{k : τ_k <= z_(k)}.  Rows of pre-scaled z."""
+    z = np.asarray(z, dtype=np.float64)
+    zs = -np.sort(-z, axis=-1)
+    fin = np.isfinite(zs)
+    zs_f = np.where(fin, zs, 0.0)
+    k = np.arange(1, z.shape[-1] + 1, dtype=np.float64)
+    mu = np.cumsum(zs_f, axis=-1) / k
+    ms = np.cumsum(zs_f * zs_f, axis=-1) / k
+    var = ms - mu * mu
+    disc = (1.0 - k * var) / k
+    with np.errstate(invalid="ignore"):
+        tau_k = mu - np.sqrt(disc)
+    cond = (disc >= 0) & (tau_k <= zs_f) & fin
+    kstar = cond.shape[-1] - np.argmax(cond[..., ::-1], axis=-1)
+    return np.take_along_axis(tau_k, (kstar - 1)[..., None], -1)[..., 0]
+
+
+def tau_bisect_exact(z: np.ndarray, alpha: float, iters: int = 200) -> np.ndarray:
+    """Exact τ for general α: Eq. 4 bisection from the Alg. 1 bracket, run until
+    the float64 bracket collapses (200 halvings of a width <= 1)."""
+    return halley_bisection(z, alpha, iters, halley=False)
+
+
+def tau_exact(z: np.ndarray, alpha: float) -> np.ndarray:
+    if alpha == 2.0:
+        return tau_sparsemax(z)
+    if alpha == 1.5:
+        return tau_entmax15(z)
+    return tau_bisect_exact(z, alpha)
+
+
+def entmax_probs(z: np.ndarray, tau: np.ndarray, alpha: float) -> np.ndarray:
+    """Eq. 2 on pre-scaled z: p = [z − τ]_+^{1/(α−1)}."""
+    return relu_pow(z - tau[..., None], 1.0 / (alpha - 1.0))
+
+
+def entmax(s: np.ndarray, alpha: float, T: int | None = None) -> np.ndarray:
+    """α-entmax of raw scores s (Eq. 2): exact τ if T is None, else the T-step
+    Halley-bisection mirror (Alg. 1)."""
+    z = (alpha - 1.0) * np.asarray(s, dtype=np.float64)
+    tau = tau_exact(z, alpha) if T is None else halley_bisection(z, alpha, T)
+    return entmax_probs(z, tau, alpha)
+
+
+def entmax_vjp(p: np.ndarray, dp: np.ndarray, alpha: float) -> np.ndarray:
+    """Sparse Jacobian-vector product:
+    J = Diag(u) − u uᵀ/‖u‖₁ with u_j = p_j^{2−α} (0 off support)."""
+    u = np.where(p > 0, np.power(np.where(p > 0, p, 1.0), 2.0 - alpha), 0.0)
+    return u * dp - (np.sum(u * dp, -1, keepdims=True) / np.sum(u, -1, keepdims=True)) * u
