@@ -148,7 +148,7 @@ def lookup_tables(M):
     return Q, K
 
 
-def attn_bwd(q, k, v, dO, tau, alpha, causal=False, scale=None, key_cols=None, use_delta=True):
+def attn_bwd(q, k, v, dO, tau, alpha, causal=False, scale=None, key_cols=None, use_delta=True, rows=None):
     """Backward pass of App. A.2, dense over rows (chunked):
       δ_i  = dO_iᵀ O⁽²⁾_i
       dP   = dO Vᵀ
@@ -157,7 +157,8 @@ def attn_bwd(q, k, v, dO, tau, alpha, causal=False, scale=None, key_cols=None, u
       dQ   = c · dS K ,  dK = c · dSᵀ Q             (× c from Eq. 1)
     ``tau`` is τ for ALL rows (the forward's τ).  ``key_cols`` restricts
     dK/dV to those key rows (row-sampled checks); dQ is then not returned.
-    ``use_delta=False`` drops δ (mutation test only)."""
+    ``use_delta=False`` drops δ (mutation test only).  ``rows`` restricts the query rows whose
+    contributions are summed (dK/dV become partial sums; bench.py's bounded CPU sample only)."""
     q = np.asarray(q, dtype=np.float64)
     k = np.asarray(k, dtype=np.float64)
     v = np.asarray(v, dtype=np.float64)
@@ -168,8 +169,8 @@ def attn_bwd(q, k, v, dO, tau, alpha, causal=False, scale=None, key_cols=None, u
     dQ = np.zeros_like(q) if key_cols is None else None
     dK = np.zeros((len(cols), d))
     dV = np.zeros((len(cols), v.shape[1]))
-    delta = np.empty(n)
-    for rc in _row_chunks(np.arange(n), k.shape[0]):
+    delta = np.zeros(n)
+    for rc in _row_chunks(np.arange(n) if rows is None else np.asarray(rows), k.shape[0]):
         p = probs(q, k, tau[rc], alpha, causal, scale, rc)
         u = u_of_p(p, alpha)
         o2 = (u @ v) / u.sum(1)[:, None]

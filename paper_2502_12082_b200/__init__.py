@@ -1,0 +1,180 @@
+"""B200-native AdaSplash α-entmax attention (arXiv 2502.12082) — Python binding.
+
+Thin marshalling layer over the C ABI in include/entmax_attn.h: every step of the hot
+path runs in the CUDA kernels of libentmax_attn.so.  PyTorch supplies device memory, the
+current CUDA stream and autograd plumbing only.  There is no CPU/eager fallback: when the
+library or a CUDA device is missing the calls raise.
+
+Public API (same names as the C ABI):
+  entmax_attn_fwd(q, k, v, alpha, causal, n_iter, scale=None, training=True) -> FwdResult
+  entmax_attn_bwd(q, k, v, d_o, fwd: FwdResult, alpha, causal, scale=None) -> (dq, dk, dv)
+  entmax_attention(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None)  (autograd op)
+q, k, v: [B, H, N, d] CUDA tensors, bf16 (tcgen05 path) or fp32 (SIMT fp32 path), same
+strides, last dim contiguous.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import EntmaxAttnError, ENTMAX_BF16, ENTMAX_FP32
+
+__all__ = ["entmax_attn_fwd", "entmax_attn_bwd", "entmax_attention", "block_size", "FwdResult",
+           "EntmaxAttnError", "impl_for", "profile_enable", "profile_reset", "profile_collect",
+           "workspace_bytes"]
+
+_DT = {torch.bfloat16: ENTMAX_BF16, torch.float32: ENTMAX_FP32}
+
+
+def block_size():
+    """(B_r, B_c): mask / lookup-table granularity of the library."""
+    br, bc = ctypes.c_int32(), ctypes.c_int32()
+    _lib.lib().entmax_attn_block_size(ctypes.byref(br), ctypes.byref(bc))
+    return br.value, bc.value
+
+
+def _shape(q: torch.Tensor) -> _lib.Shape:
+    if q.dim() != 4:
+        raise ValueError("expected [B, H, N, d] tensors")
+    B, H, N, d = q.shape
+    sb, sh, sn, sd = q.stride()
+    if sd != 1:
+        raise ValueError("last dimension must be contiguous")
+    return _lib.Shape(B, H, N, d, sb, sh, sn)
+
+
+def _check_inputs(*ts):
+    q = ts[0]
+    if not q.is_cuda:
+        raise RuntimeError("entmax_attn: tensors must be CUDA tensors (no CPU fallback)")
+    if q.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {q.dtype}")
+    for t in ts[1:]:
+        if t.shape != q.shape or t.stride() != q.stride() or t.dtype != q.dtype or t.device != q.device:
+            raise ValueError("q, k, v (and o2, dO) must share shape, strides, dtype and device")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(dev):
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def impl_for(q: torch.Tensor) -> int:
+    """1 = tcgen05 kernels, 0 = SIMT fp32 kernels, -1 = unsupported."""
+    return _lib.lib().entmax_attn_impl_for(ctypes.byref(_shape(q)), _DT[q.dtype])
+
+
+def workspace_bytes(q: torch.Tensor, causal: bool):
+    L = _lib.lib()
+    s = _shape(q)
+    return (L.entmax_attn_fwd_workspace_bytes(ctypes.byref(s), _DT[q.dtype], int(causal)),
+            L.entmax_attn_bwd_workspace_bytes(ctypes.byref(s), _DT[q.dtype], int(causal)))
+
+
+@dataclass
+class FwdResult:
+    o: torch.Tensor        # [B,H,N,d]
+    o2: torch.Tensor       # [B,H,N,d] fp32 contiguous, or None (inference)
+    tau: torch.Tensor      # [B,H,N] fp32
+    mask: torch.Tensor     # [B,H,T_r,T_c] uint8
+    row_cnt: torch.Tensor  # [B,H,T_r] int32
+    row_idx: torch.Tensor  # [B,H,T_r,T_c] int32
+
+
+def entmax_attn_fwd(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, training=True,
+                    out: FwdResult | None = None, workspace: torch.Tensor | None = None) -> FwdResult:
+    """Forward pass through the C ABI (see include/entmax_attn.h)."""
+    _check_inputs(q, k, v)
+    L = _lib.lib()
+    s = _shape(q)
+    B, H, N, d = q.shape
+    br, bc = block_size()
+    Tr, Tc = -(-N // br), -(-N // bc)
+    dev = q.device
+    if out is None:
+        out = FwdResult(
+            o=torch.empty_like(q),
+            o2=torch.empty(q.shape, dtype=torch.float32, device=dev) if training else None,
+            tau=torch.empty((B, H, N), dtype=torch.float32, device=dev),
+            mask=torch.empty((B, H, Tr, Tc), dtype=torch.uint8, device=dev),
+            row_cnt=torch.empty((B, H, Tr), dtype=torch.int32, device=dev),
+            row_idx=torch.empty((B, H, Tr, Tc), dtype=torch.int32, device=dev))
+    ws_bytes = L.entmax_attn_fwd_workspace_bytes(ctypes.byref(s), _DT[q.dtype], int(causal))
+    if workspace is None or workspace.numel() < ws_bytes:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    st = L.entmax_attn_fwd(_ptr(q), _ptr(k), _ptr(v), ctypes.byref(s), _DT[q.dtype], float(alpha),
+                           int(causal), int(n_iter), float(scale or 0.0),
+                           _ptr(out.o), _ptr(out.o2), _ptr(out.tau), _ptr(out.mask), _ptr(out.row_cnt),
+                           _ptr(out.row_idx), _ptr(workspace), ws_bytes, _stream(dev))
+    _lib.check(st, "entmax_attn_fwd")
+    return out
+
+
+def entmax_attn_bwd(q, k, v, d_o, fwd: FwdResult, alpha=1.5, causal=False, scale=None,
+                    grads=None, workspace: torch.Tensor | None = None):
+    """Backward pass through the C ABI; returns (dq, dk, dv)."""
+    if fwd.o2 is None:
+        raise ValueError("backward needs O⁽²⁾: run the forward with training=True")
+    d_o = d_o.contiguous() if d_o.stride() != q.stride() else d_o
+    _check_inputs(q, k, v, d_o)
+    if fwd.o2.dtype != torch.float32 or not fwd.o2.is_contiguous() or fwd.o2.shape != q.shape:
+        raise ValueError("o2 must be the fp32 contiguous [B,H,N,d] tensor written by entmax_attn_fwd")
+    L = _lib.lib()
+    s = _shape(q)
+    dq, dk, dv = grads if grads is not None else (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
+    ws_bytes = L.entmax_attn_bwd_workspace_bytes(ctypes.byref(s), _DT[q.dtype], int(causal))
+    if workspace is None or workspace.numel() < ws_bytes:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
+    st = L.entmax_attn_bwd(_ptr(q), _ptr(k), _ptr(v), _ptr(fwd.o2), _ptr(d_o), _ptr(fwd.tau), _ptr(fwd.mask),
+                           _ptr(fwd.row_cnt), _ptr(fwd.row_idx), ctypes.byref(s), _DT[q.dtype], float(alpha),
+                           int(causal), float(scale or 0.0), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(workspace),
+                           ws_bytes, _stream(q.device))
+    _lib.check(st, "entmax_attn_bwd")
+    return dq, dk, dv
+
+
+class _EntmaxAttention(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, q, k, v, alpha, causal, n_iter, scale):
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        fw = entmax_attn_fwd(q, k, v, alpha, causal, n_iter, scale, training=True)
+        ctx.save_for_backward(q, k, v, fw.o2, fw.tau, fw.mask, fw.row_cnt, fw.row_idx)
+        ctx.cfg = (alpha, causal, scale)
+        return fw.o
+
+    @staticmethod
+    def backward(ctx, d_o):
+        q, k, v, o2, tau, mask, row_cnt, row_idx = ctx.saved_tensors
+        alpha, causal, scale = ctx.cfg
+        fw = FwdResult(None, o2, tau, mask, row_cnt, row_idx)
+        dq, dk, dv = entmax_attn_bwd(q, k, v, d_o.contiguous(), fw, alpha, causal, scale)
+        return dq, dk, dv, None, None, None, None
+
+
+def entmax_attention(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None):
+    """α-entmax attention O = entmax_α(QKᵀ/√d) V with AdaSplash block skipping (autograd op)."""
+    return _EntmaxAttention.apply(q, k, v, alpha, causal, n_iter, scale)
+
+
+def profile_enable(on: bool = True):
+    _lib.lib().entmax_attn_profile_enable(int(on))
+
+
+def profile_reset():
+    _lib.lib().entmax_attn_profile_reset()
+
+
+def profile_collect():
+    """{kernel name: (launches, total_ms)} since the last reset (synchronises the events)."""
+    cap = 64
+    names = (ctypes.c_char_p * cap)()
+    launches = (ctypes.c_int32 * cap)()
+    ms = (ctypes.c_double * cap)()
+    n = _lib.lib().entmax_attn_profile_collect(names, launches, ms, cap)
+    return {names[i].decode(): (launches[i], ms[i]) for i in range(n)}

@@ -1,0 +1,164 @@
+// common.cuh — per-element α-entmax arithmetic and the Alg. 1 row update, shared by the
+// SIMT and the tcgen05 kernels of this library (never by the oracle).
+//
+// Exponent e = 1/(α−1).  The three α of the paper's configs give integer e:
+//   α = 2    → e = 1 (sparsemax),  α = 1.5 → e = 2,  α = 1.25 → e = 4.
+// They are compile-time specialisations (E = 1, 2, 4); E = 0 is the generic-α path that uses
+// exp2/log2.  All arithmetic is fp32.
+#pragma once
+
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace entmax {
+
+constexpr int kBr = 128;  // query rows per block  (mask granularity B_r)
+constexpr int kBc = 128;  // keys per block         (mask granularity B_c)
+
+struct AlphaParams {
+  float alpha;   // α
+  float e;       // 1/(α−1)
+  float em1;     // e − 1   (= (2−α)/(α−1); exponent of U = P^{2−α})
+  float em2;     // e − 2
+  float c1;      // −e               (f' = c1 · Σ[x]_+^{e−1},  Eq. 6)
+  float c2;      // (2−α)/(α−1)²     (f'' = c2 · Σ[x]_+^{e−2}, Eq. 7)
+  float cp;      // (α−1)·scale: z = cp · s_raw  (Alg. 1 line 3 with Eq. 1 scale)
+  float scale;   // c = 1/√d or user value
+};
+
+inline AlphaParams make_alpha_params(float alpha, float scale) {
+  AlphaParams a;
+  a.alpha = alpha;
+  a.e = 1.0f / (alpha - 1.0f);
+  a.em1 = a.e - 1.0f;
+  a.em2 = a.e - 2.0f;
+  a.c1 = -a.e;
+  a.c2 = (2.0f - alpha) / ((alpha - 1.0f) * (alpha - 1.0f));
+  a.cp = (alpha - 1.0f) * scale;
+  a.scale = scale;
+  return a;
+}
+
+// Exponent code dispatched at launch: 1, 2, 4 or 0 (generic).
+inline int exponent_code(float alpha) {
+  if (alpha == 2.0f) return 1;
+  if (alpha == 1.5f) return 2;
+  if (alpha == 1.25f) return 4;
+  return 0;
+}
+
+__device__ __forceinline__ float gpow(float x, float p) {  // x > 0
+  return exp2f(p * __log2f(x));
+}
+
+// Accumulate the three sums of Eq. 3 / Eq. 6 / Eq. 7 for one element x = z − τ:
+//   a0 += [x]_+^e,  a1 += [x]_+^{e−1},  a2 += [x]_+^{e−2}   ([x]_+^p := 0 for x <= 0, reading c7)
+template <int E>
+__device__ __forceinline__ void accum_f(float x, const AlphaParams& ap, float& a0, float& a1, float& a2) {
+  if (E == 1) {
+    float xp = fmaxf(x, 0.f);
+    a0 += xp;
+    a1 += (x > 0.f) ? 1.f : 0.f;
+  } else if (E == 2) {
+    float xp = fmaxf(x, 0.f);
+    a0 = fmaf(xp, xp, a0);
+    a1 += xp;
+    a2 += (x > 0.f) ? 1.f : 0.f;
+  } else if (E == 4) {
+    float xp = fmaxf(x, 0.f);
+    float x2 = xp * xp;
+    a0 = fmaf(x2, x2, a0);
+    a1 = fmaf(x2, xp, a1);
+    a2 += x2;
+  } else {
+    if (x > 0.f) {
+      float l = __log2f(x);
+      a0 += exp2f(ap.e * l);
+      a1 += exp2f(ap.em1 * l);
+      a2 += exp2f(ap.em2 * l);
+    }
+  }
+}
+
+// P = [x]_+^e (Eq. 2) and U = P^{2−α} = [x]_+^{e−1} (P:L377, 0 off the support).
+template <int E>
+__device__ __forceinline__ void p_and_u(float x, const AlphaParams& ap, float& p, float& u) {
+  if (E == 1) {
+    p = fmaxf(x, 0.f);
+    u = (x > 0.f) ? 1.f : 0.f;
+  } else if (E == 2) {
+    u = fmaxf(x, 0.f);
+    p = u * u;
+  } else if (E == 4) {
+    float xp = fmaxf(x, 0.f);
+    float x2 = xp * xp;
+    u = x2 * xp;
+    p = x2 * x2;
+  } else {
+    if (x > 0.f) {
+      float l = __log2f(x);
+      p = exp2f(ap.e * l);
+      u = exp2f(ap.em1 * l);
+    } else {
+      p = 0.f;
+      u = 0.f;
+    }
+  }
+}
+
+// Alg. 1 state of one row.
+struct RowState {
+  float lo, hi, tau;
+};
+
+// Alg. 1 lines 4-6: τ_lo = m − 1, τ_hi = m − n^{1−α}, τ = midpoint.
+__device__ __forceinline__ RowState bracket_init(float zmax, float n_visible, float alpha) {
+  RowState s;
+  s.lo = zmax - 1.0f;
+  s.hi = zmax - exp2f((1.0f - alpha) * __log2f(n_visible));
+  s.tau = 0.5f * (s.lo + s.hi);
+  return s;
+}
+
+// One Alg. 1 iteration given the accumulated sums at the current τ (lines 8-14):
+// bracket update (Eq. 4, tie f = 0 → τ_lo = τ), Halley candidate (Eq. 5), accept iff it lies in
+// the updated bracket (inclusive) and is finite, else midpoint.
+__device__ __forceinline__ void alg1_update(RowState& s, float a0, float a1, float a2, const AlphaParams& ap) {
+  float f = a0 - 1.0f;         // Eq. 3
+  float f1 = ap.c1 * a1;       // Eq. 6
+  float f2 = ap.c2 * a2;       // Eq. 7
+  if (f < 0.f) s.hi = s.tau; else s.lo = s.tau;
+  float den = 2.0f * f1 * f1 - f * f2;
+  float th = s.tau - 2.0f * f * f1 / den;
+  bool ok = (den != 0.f) && isfinite(th) && th >= s.lo && th <= s.hi;
+  s.tau = ok ? th : 0.5f * (s.lo + s.hi);
+}
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Geometry of one call, passed by value to every kernel.
+struct Geom {
+  int B, H, N, d;
+  long long sb, sh, sn;   // element strides of [B,H,N,d] tensors
+  int Tr, Tc;             // ⌈N/B_r⌉, ⌈N/B_c⌉
+  int causal;
+  __host__ __device__ long long head_off(int bh) const {
+    int b = bh / H, h = bh - (bh / H) * H;
+    return (long long)b * sb + (long long)h * sh;
+  }
+  // number of key blocks visible to query block i (causal: blocks j with j*Bc <= last row of i)
+  __host__ __device__ int visible_kblocks(int i) const {
+    if (!causal) return Tc;
+    int last_row = min(N, (i + 1) * kBr) - 1;
+    return last_row / kBc + 1;
+  }
+};
+
+}  // namespace entmax

@@ -1,0 +1,324 @@
+// simt_kernels.cuh — FP32-arithmetic SIMT kernels for the whole hot path.
+//
+// Used for fp32 inputs (config 1 of BASELINE.json needs true-fp32 scores to meet the 1e-4
+// bar; tf32 tensor cores give ~5e-3) and for head dims the tcgen05 kernels do
+// not cover.  One thread owns one query row (τ, forward output, dQ) or one key row (dK/dV);
+// K/V (or Q/dO) tiles are staged in shared memory and read as broadcasts.  Same block
+// geometry (B_r = B_c = 128) and the same mask/table semantics as the tcgen05 kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace entmax {
+namespace simt {
+
+template <int D>
+struct Tile {
+  static constexpr int KT = (4096 / D) < 128 ? (4096 / D) : 128;  // rows per staged tile
+};
+
+// Stage rows [r0, r0+KT) of a [N,d] head (row stride sn) into smem as fp32, zero past N.
+template <typename T, int D>
+__device__ __forceinline__ void stage_rows(float (*dst)[D], const T* src, long long sn, int r0, int N) {
+  constexpr int KT = Tile<D>::KT;
+  for (int idx = threadIdx.x; idx < KT * D; idx += blockDim.x) {
+    int rr = idx / D, cc = idx - (idx / D) * D;
+    int row = r0 + rr;
+    dst[rr][cc] = (row < N) ? to_f<T>(src[(long long)row * sn + cc]) : 0.f;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ float dot_row(const float* a, const float* b) {
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < D; ++c) s = fmaf(a[c], b[c], s);
+  return s;
+}
+
+// τ per query row: pass 0 = row max, then T passes of Alg. 1 over all visible keys (Alg. 3).
+template <typename T, int D, int E>
+__global__ void __launch_bounds__(128) tau_kernel(const T* __restrict__ q, const T* __restrict__ k, Geom g,
+                                                  AlphaParams ap, int n_iter, float* __restrict__ tau_out) {
+  constexpr int KT = Tile<D>::KT;
+  __shared__ float ks[KT][D];
+  const int i = blockIdx.x, bh = blockIdx.y;
+  const int r = i * kBr + threadIdx.x;
+  const bool valid = r < g.N;
+  const T* qh = q + g.head_off(bh);
+  const T* kh = k + g.head_off(bh);
+  float qr[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) qr[c] = valid ? to_f<T>(qh[(long long)r * g.sn + c]) : 0.f;
+  const int kend = g.causal ? min(g.N, (i + 1) * kBr) : g.N;
+  const int my_last = g.causal ? r : g.N - 1;
+
+  float smax = -INFINITY;
+  for (int kt = 0; kt < kend; kt += KT) {
+    __syncthreads();
+    stage_rows<T, D>(ks, kh, g.sn, kt, kend);
+    __syncthreads();
+    const int jn = min(KT, kend - kt);
+    for (int j = 0; j < jn; ++j)
+      if (kt + j <= my_last) smax = fmaxf(smax, dot_row<D>(qr, ks[j]));
+  }
+  const float n_vis = g.causal ? (float)(r + 1) : (float)g.N;
+  RowState st = bracket_init(smax * ap.cp, n_vis, ap.alpha);
+  for (int t = 0; t < n_iter; ++t) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+    for (int kt = 0; kt < kend; kt += KT) {
+      __syncthreads();
+      stage_rows<T, D>(ks, kh, g.sn, kt, kend);
+      __syncthreads();
+      const int jn = min(KT, kend - kt);
+      for (int j = 0; j < jn; ++j) {
+        if (kt + j <= my_last) {
+          float x = fmaf(dot_row<D>(qr, ks[j]), ap.cp, -st.tau);
+          accum_f<E>(x, ap, a0, a1, a2);
+        }
+      }
+    }
+    alg1_update(st, a0, a1, a2, ap);
+  }
+  if (valid) tau_out[(long long)bh * g.N + r] = st.tau;
+}
+
+// Output pass over every visible key block; decides M_ij exactly (any x > 0), writes the mask
+// row, the 𝒬_i table, O and O⁽²⁾.
+template <typename T, int D, int E>
+__global__ void __launch_bounds__(128) out_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                  const T* __restrict__ v, Geom g, AlphaParams ap,
+                                                  const float* __restrict__ tau, T* __restrict__ o,
+                                                  float* __restrict__ o2, uint8_t* __restrict__ mask,
+                                                  int32_t* __restrict__ row_cnt, int32_t* __restrict__ row_idx) {
+  constexpr int KT = Tile<D>::KT;
+  __shared__ float ks[KT][D];
+  __shared__ float vs[KT][D];
+  const int i = blockIdx.x, bh = blockIdx.y;
+  const int r = i * kBr + threadIdx.x;
+  const bool valid = r < g.N;
+  const long long hoff = g.head_off(bh);
+  const T* qh = q + hoff;
+  const T* kh = k + hoff;
+  const T* vh = v + hoff;
+  float qr[D], oa[D], o2a[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    qr[c] = valid ? to_f<T>(qh[(long long)r * g.sn + c]) : 0.f;
+    oa[c] = 0.f;
+    o2a[c] = 0.f;
+  }
+  const float tr = valid ? tau[(long long)bh * g.N + r] : 0.f;
+  const int my_last = g.causal ? r : g.N - 1;
+  const int nkb = g.visible_kblocks(i);
+  float usum = 0.f;
+  int cnt = 0;
+  uint8_t* mrow = mask + ((long long)bh * g.Tr + i) * g.Tc;
+  int32_t* lrow = row_idx + ((long long)bh * g.Tr + i) * g.Tc;
+  for (int jb = 0; jb < nkb; ++jb) {
+    bool act = false;
+    for (int kt = jb * kBc; kt < min(g.N, (jb + 1) * kBc); kt += KT) {
+      __syncthreads();
+      stage_rows<T, D>(ks, kh, g.sn, kt, g.N);
+      stage_rows<T, D>(vs, vh, g.sn, kt, g.N);
+      __syncthreads();
+      const int jn = min(KT, g.N - kt);
+      for (int j = 0; j < jn; ++j) {
+        if (valid && kt + j <= my_last) {
+          float x = fmaf(dot_row<D>(qr, ks[j]), ap.cp, -tr);
+          if (x > 0.f) {
+            float p, u;
+            p_and_u<E>(x, ap, p, u);
+            act = true;
+            usum += u;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              oa[c] = fmaf(p, vs[j][c], oa[c]);
+              o2a[c] = fmaf(u, vs[j][c], o2a[c]);
+            }
+          }
+        }
+      }
+    }
+    const int any = __syncthreads_or(act ? 1 : 0);
+    if (threadIdx.x == 0) {
+      mrow[jb] = any ? 1 : 0;
+      if (any) lrow[cnt++] = jb;
+    }
+  }
+  for (int jb = nkb + threadIdx.x; jb < g.Tc; jb += blockDim.x) mrow[jb] = 0;
+  if (threadIdx.x == 0) row_cnt[(long long)bh * g.Tr + i] = cnt;
+  if (valid) {
+    T* orow = o + hoff + (long long)r * g.sn;
+#pragma unroll
+    for (int c = 0; c < D; ++c) orow[c] = from_f<T>(oa[c]);
+    if (o2 != nullptr) {
+      float* o2row = o2 + ((long long)bh * g.N + r) * D;   // fp32, contiguous
+      const float inv = 1.0f / usum;
+#pragma unroll
+      for (int c = 0; c < D; ++c) o2row[c] = o2a[c] * inv;
+    }
+  }
+}
+
+// dK_j, dV_j over 𝒦_j (Alg. 4): one thread per key row.
+template <typename T, int D, int E>
+__global__ void __launch_bounds__(128) dkdv_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                   const T* __restrict__ v, const T* __restrict__ dO, Geom g,
+                                                   AlphaParams ap, const float* __restrict__ tau,
+                                                   const float* __restrict__ delta,
+                                                   const int32_t* __restrict__ col_cnt,
+                                                   const int32_t* __restrict__ col_idx, T* __restrict__ dk,
+                                                   T* __restrict__ dv) {
+  constexpr int KT = Tile<D>::KT;
+  __shared__ float qs[KT][D];
+  __shared__ float ds_[KT][D];
+  __shared__ float ts[KT], dls[KT];
+  const int jb = blockIdx.x, bh = blockIdx.y;
+  const int key = jb * kBc + threadIdx.x;
+  const bool valid = key < g.N;
+  const long long hoff = g.head_off(bh);
+  float kr[D], vr[D], dka[D], dva[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    kr[c] = valid ? to_f<T>(k[hoff + (long long)key * g.sn + c]) : 0.f;
+    vr[c] = valid ? to_f<T>(v[hoff + (long long)key * g.sn + c]) : 0.f;
+    dka[c] = 0.f;
+    dva[c] = 0.f;
+  }
+  const int cnt = col_cnt[(long long)bh * g.Tc + jb];
+  const int32_t* lst = col_idx + ((long long)bh * g.Tc + jb) * g.Tr;
+  for (int t = 0; t < cnt; ++t) {
+    const int ib = lst[t];
+    for (int rt = ib * kBr; rt < min(g.N, (ib + 1) * kBr); rt += KT) {
+      __syncthreads();
+      stage_rows<T, D>(qs, q + hoff, g.sn, rt, g.N);
+      stage_rows<T, D>(ds_, dO + hoff, g.sn, rt, g.N);
+      for (int x = threadIdx.x; x < KT; x += blockDim.x) {
+        int row = rt + x;
+        ts[x] = row < g.N ? tau[(long long)bh * g.N + row] : 0.f;
+        dls[x] = row < g.N ? delta[(long long)bh * g.N + row] : 0.f;
+      }
+      __syncthreads();
+      const int rn = min(KT, g.N - rt);
+      for (int rr = 0; rr < rn; ++rr) {
+        const int row = rt + rr;
+        if (valid && (!g.causal || key <= row)) {
+          float x = fmaf(dot_row<D>(qs[rr], kr), ap.cp, -ts[rr]);
+          if (x > 0.f) {
+            float p, u;
+            p_and_u<E>(x, ap, p, u);
+            float dp = dot_row<D>(ds_[rr], vr);
+            float dsv = u * (dp - dls[rr]);
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              dva[c] = fmaf(p, ds_[rr][c], dva[c]);
+              dka[c] = fmaf(dsv, qs[rr][c], dka[c]);
+            }
+          }
+        }
+      }
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+      dk[hoff + (long long)key * g.sn + c] = from_f<T>(dka[c] * ap.scale);
+      dv[hoff + (long long)key * g.sn + c] = from_f<T>(dva[c]);
+    }
+  }
+}
+
+// dQ_i over 𝒬_i (Alg. 5): one thread per query row.
+template <typename T, int D, int E>
+__global__ void __launch_bounds__(128) dq_kernel(const T* __restrict__ q, const T* __restrict__ k,
+                                                 const T* __restrict__ v, const T* __restrict__ dO, Geom g,
+                                                 AlphaParams ap, const float* __restrict__ tau,
+                                                 const float* __restrict__ delta, const int32_t* __restrict__ row_cnt,
+                                                 const int32_t* __restrict__ row_idx, T* __restrict__ dq) {
+  constexpr int KT = Tile<D>::KT;
+  __shared__ float ks[KT][D];
+  __shared__ float vs[KT][D];
+  const int ib = blockIdx.x, bh = blockIdx.y;
+  const int row = ib * kBr + threadIdx.x;
+  const bool valid = row < g.N;
+  const long long hoff = g.head_off(bh);
+  float qr[D], dor[D], dqa[D];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    qr[c] = valid ? to_f<T>(q[hoff + (long long)row * g.sn + c]) : 0.f;
+    dor[c] = valid ? to_f<T>(dO[hoff + (long long)row * g.sn + c]) : 0.f;
+    dqa[c] = 0.f;
+  }
+  const float tr = valid ? tau[(long long)bh * g.N + row] : 0.f;
+  const float dl = valid ? delta[(long long)bh * g.N + row] : 0.f;
+  const int cnt = row_cnt[(long long)bh * g.Tr + ib];
+  const int32_t* lst = row_idx + ((long long)bh * g.Tr + ib) * g.Tc;
+  for (int t = 0; t < cnt; ++t) {
+    const int jb = lst[t];
+    for (int kt = jb * kBc; kt < min(g.N, (jb + 1) * kBc); kt += KT) {
+      __syncthreads();
+      stage_rows<T, D>(ks, k + hoff, g.sn, kt, g.N);
+      stage_rows<T, D>(vs, v + hoff, g.sn, kt, g.N);
+      __syncthreads();
+      const int jn = min(KT, g.N - kt);
+      for (int j = 0; j < jn; ++j) {
+        if (valid && (!g.causal || kt + j <= row)) {
+          float x = fmaf(dot_row<D>(qr, ks[j]), ap.cp, -tr);
+          if (x > 0.f) {
+            float p, u;
+            p_and_u<E>(x, ap, p, u);
+            float dp = dot_row<D>(dor, vs[j]);
+            float dsv = u * (dp - dl);
+#pragma unroll
+            for (int c = 0; c < D; ++c) dqa[c] = fmaf(dsv, ks[j][c], dqa[c]);
+          }
+        }
+      }
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int c = 0; c < D; ++c) dq[hoff + (long long)row * g.sn + c] = from_f<T>(dqa[c] * ap.scale);
+  }
+}
+
+}  // namespace simt
+
+// ---------------------------------------------------------------------------------------
+// Kernels shared by both implementations
+// ---------------------------------------------------------------------------------------
+
+// δ_i = dO_iᵀ O⁽²⁾_i: one warp per row, fp32 accumulation.
+template <typename T>
+__global__ void delta_kernel(const T* __restrict__ dO, const float* __restrict__ o2, Geom g, float* __restrict__ delta) {
+  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long total = (long long)g.B * g.H * g.N;
+  if (warp >= total) return;
+  const int bh = (int)(warp / g.N);
+  const int r = (int)(warp - (long long)bh * g.N);
+  const long long off = g.head_off(bh) + (long long)r * g.sn;
+  const float* o2r = o2 + warp * g.d;   // fp32 contiguous [B,H,N,d]
+  float s = 0.f;
+  for (int c = lane; c < g.d; c += 32) s = fmaf(to_f<T>(dO[off + c]), o2r[c], s);
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  if (lane == 0) delta[warp] = s;
+}
+
+// 𝒦_j = {i | M_ij = 1} from the mask, increasing i; one thread per (head, j).
+__global__ void col_lists_kernel(const uint8_t* __restrict__ mask, int BH, int Tr, int Tc,
+                                 int32_t* __restrict__ col_cnt, int32_t* __restrict__ col_idx) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)BH * Tc) return;
+  const int bh = (int)(t / Tc), j = (int)(t - (long long)(t / Tc) * Tc);
+  const uint8_t* m = mask + (long long)bh * Tr * Tc + j;
+  int32_t* out = col_idx + ((long long)bh * Tc + j) * Tr;
+  int cnt = 0;
+  for (int i = 0; i < Tr; ++i)
+    if (m[(long long)i * Tc]) out[cnt++] = i;
+  col_cnt[t] = cnt;
+}
+
+}  // namespace entmax

@@ -1,0 +1,155 @@
+// sm100.cu — host launchers of the tcgen05 / TMEM / TMA kernels (sm100_kernels.cuh).
+#include "entmax_attn.h"
+#include "runtime.h"
+#include "sm100_kernels.cuh"
+#include "tmap.h"
+
+namespace entmax {
+namespace sm100 {
+namespace {
+
+template <int D>
+constexpr size_t tau_smem(int Tc) {
+  return 1024 + Cfg<D>::TILE + ((D == 64) ? 4 : 3) * Cfg<D>::TILE + (size_t)Tc;
+}
+template <int D>
+constexpr size_t out_smem(int Tc) {
+  return 1024 + Cfg<D>::TILE + ((D == 64) ? 3 : 2) * 2 * Cfg<D>::TILE + 65536 + (size_t)Tc;
+}
+template <int D>
+constexpr size_t dkdv_smem() {
+  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 2 : 1) * (2 * Cfg<D>::TILE + 1024) + 65536;
+}
+template <int D>
+constexpr size_t dq_smem() {
+  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 2 : 1) * 2 * Cfg<D>::TILE + 32768;
+}
+
+constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
+
+template <typename K>
+int set_smem(K kernel, size_t bytes) {
+  if (bytes > kMaxSmem) return fail(ENTMAX_ERR_UNSUPPORTED, "kernel needs %zu B of shared memory", bytes);
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return fail(ENTMAX_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+  return ENTMAX_OK;
+}
+
+int tmaps(const Geom& g, std::initializer_list<std::pair<CUtensorMap*, const void*>> maps) {
+  for (auto& m : maps)
+    if (!make_tmap_bhnd(m.first, m.second, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn))
+      return fail(ENTMAX_ERR_INVALID_ARG, "cuTensorMapEncodeTiled failed (alignment/strides?)");
+  return ENTMAX_OK;
+}
+
+template <int D, int E>
+int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const AlphaParams& ap, int n_iter, void* o,
+          void* o2, float* tau, uint8_t* mask, int32_t* row_cnt, int32_t* row_idx, int32_t* cand_cnt,
+          int32_t* cand_idx, cudaStream_t st) {
+  CUtensorMap tq, tk, tv;
+  if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}})) return rc;
+  const dim3 grid(g.Tr, g.B * g.H);
+  {
+    const size_t sm = tau_smem<D>(g.Tc);
+    if (int rc = set_smem(tau_kernel<D, E>, sm)) return rc;
+    ProfScope ps("tau_sm100", st);
+    tau_kernel<D, E><<<grid, kThreads, sm, st>>>(tq, tk, g, ap, n_iter, tau, cand_cnt, cand_idx);
+  }
+  if (int rc = cuda_status("tau_sm100")) return rc;
+  const size_t sm = out_smem<D>(g.Tc);
+  if (o2 != nullptr) {
+    if (int rc = set_smem(out_kernel<D, E, true>, sm)) return rc;
+    ProfScope ps("out_sm100", st);
+    out_kernel<D, E, true><<<grid, kThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
+                                                       (__nv_bfloat16*)o, (float*)o2, mask, row_cnt, row_idx);
+  } else {
+    if (int rc = set_smem(out_kernel<D, E, false>, sm)) return rc;
+    ProfScope ps("out_sm100", st);
+    out_kernel<D, E, false><<<grid, kThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
+                                                        (__nv_bfloat16*)o, nullptr, mask, row_cnt, row_idx);
+  }
+  return cuda_status("out_sm100");
+}
+
+template <int D, int E>
+int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap,
+          const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx,
+          const int32_t* col_cnt, const int32_t* col_idx, void* dq, void* dk, void* dv, cudaStream_t st) {
+  CUtensorMap tq, tk, tv, tdo;
+  if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
+  {
+    const size_t sm = dkdv_smem<D>();
+    if (int rc = set_smem(dkdv_kernel<D, E>, sm)) return rc;
+    ProfScope ps("dkdv_sm100", st);
+    dkdv_kernel<D, E><<<dim3(g.Tc, g.B * g.H), kThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, col_cnt,
+                                                                     col_idx, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
+  }
+  if (int rc = cuda_status("dkdv_sm100")) return rc;
+  {
+    const size_t sm = dq_smem<D>();
+    if (int rc = set_smem(dq_kernel<D, E>, sm)) return rc;
+    ProfScope ps("dq_sm100", st);
+    dq_kernel<D, E><<<dim3(g.Tr, g.B * g.H), kThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, row_cnt, row_idx,
+                                                                   (__nv_bfloat16*)dq);
+  }
+  return cuda_status("dq_sm100");
+}
+
+template <template <int, int> class Op, typename... A>
+int dispatch(int d, int ecode, A&&... a) {
+#define ENTMAX_E(DD)                                   \
+  switch (ecode) {                                     \
+    case 1: return Op<DD, 1>::run(a...);               \
+    case 2: return Op<DD, 2>::run(a...);               \
+    case 4: return Op<DD, 4>::run(a...);               \
+    default: return Op<DD, 0>::run(a...);              \
+  }
+  if (d == 64) ENTMAX_E(64)
+  if (d == 128) ENTMAX_E(128)
+#undef ENTMAX_E
+  return fail(ENTMAX_ERR_UNSUPPORTED, "tcgen05 path supports d in {64, 128} (got %d)", d);
+}
+
+template <int D, int E>
+struct FwdOp {
+  template <typename... A>
+  static int run(A&&... a) { return fwd_t<D, E>(a...); }
+};
+template <int D, int E>
+struct BwdOp {
+  template <typename... A>
+  static int run(A&&... a) { return bwd_t<D, E>(a...); }
+};
+
+}  // namespace
+
+bool available() {
+  static const bool ok = [] {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return major == 10 && minor == 0 && tmap_encoder() != nullptr;
+  }();
+  return ok;
+}
+
+int fwd(const void* q, const void* k, const void* v, const Geom& g, const AlphaParams& ap, int ecode, int n_iter,
+        void* o, void* o2, float* tau, uint8_t* mask, int32_t* row_cnt, int32_t* row_idx, int32_t* cand_cnt,
+        int32_t* cand_idx, cudaStream_t st) {
+  return dispatch<FwdOp>(g.d, ecode, q, k, v, g, ap, n_iter, o, o2, tau, mask, row_cnt, row_idx, cand_cnt, cand_idx,
+                         st);
+}
+
+int bwd(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap, int ecode,
+        const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx, const int32_t* col_cnt,
+        const int32_t* col_idx, void* dq, void* dk, void* dv, cudaStream_t st) {
+  return dispatch<BwdOp>(g.d, ecode, q, k, v, dO, g, ap, tau, delta, row_cnt, row_idx, col_cnt, col_idx, dq, dk, dv,
+                         st);
+}
+
+}  // namespace sm100
+}  // namespace entmax

@@ -10,12 +10,17 @@ any code.  Recipes (DESIGN.md §"Input recipe"):
 * ``gaussian``  — the paper's efficiency-benchmark generator: Q ~ N(0, σ²=6),
   K, V, dO ~ N(0, 1) ("σ² = 6 of query vectors").
 * ``planted``   — planted block sparsity for the Fig. 1 "runtime vs input
-  sparsity" sweep.  Each query block is
-  assigned a cluster direction u_c; each cluster owns m = max(1, round(ρ·T_c))
-  key blocks; Q rows and owned K rows are a·u_c + 0.02·N(0,1), dead K rows are
-  N(0,1).  With a = sqrt(gap·sqrt(d)) matching scores sit at ≈ gap after the
-  1/√d scale, dead scores at ≈ N(0, gap/√d), so the realised block density is
-  the target ρ and block margins are large.
+  sparsity" sweep (modified).  Each query block
+  is assigned a cluster direction u_c; each cluster owns m = max(1, round(ρ·T_c))
+  key blocks (C <= 8 clusters).  Q rows are a·u_c + ε_q with ε_q ~ N(0, σ_q²=6)
+  projected orthogonally to every cluster direction; owned K rows are a·u_c + N(0,1); dead K rows are N(0,1).
+  With a = sqrt(gap·sqrt(d)) the scores of a query against its owned keys are
+  gap + N(0, ≈7.4) after the 1/√d scale, against dead keys N(0, ≈7.4): inside
+  the owned blocks the rows look like the paper's Gaussian benchmark (a few
+  support keys per row, spread over all owned blocks), the dead blocks sit far
+  below τ, so the realised block density is the target ρ with large margins.
+  Keys keep a Gaussian spread around their cluster direction (a near-constant
+  key set would make dQ = Σ dS·K a near-total cancellation).
 
 Every head (b, h) is drawn from its own stream seeded by (seed, b, h), so a rank
 that owns a slice of heads regenerates exactly its slice.
@@ -45,7 +50,7 @@ def gaussian_head(N: int, d: int, seed: int, b: int = 0, h: int = 0, sigma2_q: f
 
 
 def planted_head(N: int, d: int, rho: float, seed: int, b: int = 0, h: int = 0,
-                 Br: int = 128, Bc: int = 128, gap: float = 12.0, noise: float = 0.02):
+                 Br: int = 128, Bc: int = 128, gap: float = 12.0, sigma2_q: float = 6.0):
     """Planted block-sparse head.  Returns (q, k, v, do, owned) where
     ``owned[i_block]`` is the sorted array of key blocks planted for query block i.
     Only generator structure lives here; which blocks are *active* is decided by the
@@ -55,7 +60,7 @@ def planted_head(N: int, d: int, rho: float, seed: int, b: int = 0, h: int = 0,
     Tc = (N + Bc - 1) // Bc
     m = max(1, int(round(rho * Tc)))
     m = min(m, Tc)
-    C = max(1, min(d, Tc // m, Tr))
+    C = max(1, min(8, d // 4, Tc // m, Tr))          # few clusters: noise keeps d − C free dims
     # orthonormal cluster directions (columns of a random orthogonal matrix)
     g = rng.standard_normal((d, d))
     qmat, _ = np.linalg.qr(g)
@@ -67,7 +72,9 @@ def planted_head(N: int, d: int, rho: float, seed: int, b: int = 0, h: int = 0,
     q = np.empty((N, d), dtype=np.float64)
     for i in range(Tr):
         r0, r1 = i * Br, min(N, (i + 1) * Br)
-        q[r0:r1] = a * u[qc[i]] + noise * rng.standard_normal((r1 - r0, d))
+        eps = np.sqrt(sigma2_q) * rng.standard_normal((r1 - r0, d))
+        eps -= (eps @ u.T) @ u                     # keep the query noise off every cluster axis
+        q[r0:r1] = a * u[qc[i]] + eps
     k = rng.standard_normal((N, d))
     owner = np.full(Tc, -1)
     for c in range(C):
@@ -75,7 +82,7 @@ def planted_head(N: int, d: int, rho: float, seed: int, b: int = 0, h: int = 0,
     for j in range(Tc):
         if owner[j] >= 0:
             c0, c1 = j * Bc, min(N, (j + 1) * Bc)
-            k[c0:c1] = a * u[owner[j]] + noise * rng.standard_normal((c1 - c0, d))
+            k[c0:c1] += a * u[owner[j]]
     v = rng.standard_normal((N, d))
     do = rng.standard_normal((N, d))
     owned = [cluster_blocks[qc[i]] for i in range(Tr)]

@@ -1,0 +1,85 @@
+"""The C-ABI library loads on a CPU-only box and exports every symbol that
+include/entmax_attn.h declares; host-side validation paths work without a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2502_12082_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "entmax_attn.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(entmax_attn_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = _declared()
+    for must in ("entmax_attn_fwd", "entmax_attn_bwd", "entmax_attn_block_size",
+                 "entmax_attn_fwd_workspace_bytes", "entmax_attn_bwd_workspace_bytes",
+                 "entmax_attn_status_string", "entmax_attn_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    for name in _declared():
+        assert hasattr(L, name), name
+
+
+def test_status_strings_and_block_size():
+    L = _lib.lib()
+    assert L.entmax_attn_status_string(0) == b"ok"
+    assert L.entmax_attn_status_string(3) == b"workspace too small"
+    br, bc = ctypes.c_int32(), ctypes.c_int32()
+    L.entmax_attn_block_size(ctypes.byref(br), ctypes.byref(bc))
+    assert (br.value, bc.value) == (128, 128)
+
+
+def test_workspace_sizes_scale_with_blocks():
+    L = _lib.lib()
+    s = _lib.Shape(4, 12, 8192, 64, 12 * 8192 * 64, 8192 * 64, 64)
+    fw = L.entmax_attn_fwd_workspace_bytes(ctypes.byref(s), 0, 0)
+    bw = L.entmax_attn_bwd_workspace_bytes(ctypes.byref(s), 0, 0)
+    BH, T = 48, 64
+    assert fw >= BH * T * 4 + BH * T * T * 4
+    assert bw >= BH * 8192 * 4 + BH * T * 4 + BH * T * T * 4
+
+
+@pytest.mark.parametrize("alpha,n_iter,status", [(1.0, 3, 1), (0.5, 3, 1), (2.5, 3, 2), (1.5, 0, 1)])
+def test_fwd_rejects_bad_arguments_before_launch(alpha, n_iter, status):
+    L = _lib.lib()
+    s = _lib.Shape(1, 1, 256, 64, 256 * 64, 256 * 64, 64)
+    fake = ctypes.c_void_p(0x10000)  # never dereferenced: validation fails first
+    rc = L.entmax_attn_fwd(fake, fake, fake, ctypes.byref(s), 0, alpha, 0, n_iter, 0.0,
+                           fake, fake, fake, fake, fake, fake, fake, 1 << 30, None)
+    assert rc == status
+    assert L.entmax_attn_last_error()
+
+
+def test_fwd_rejects_small_workspace_and_bad_strides():
+    L = _lib.lib()
+    fake = ctypes.c_void_p(0x10000)
+    s = _lib.Shape(1, 1, 256, 64, 256 * 64, 256 * 64, 64)
+    rc = L.entmax_attn_fwd(fake, fake, fake, ctypes.byref(s), 0, 1.5, 0, 3, 0.0,
+                           fake, fake, fake, fake, fake, fake, fake, 16, None)
+    assert rc == _lib.ENTMAX_ERR_WORKSPACE
+    bad = _lib.Shape(1, 1, 256, 64, 256 * 64, 256 * 64, 60)   # rows overlap
+    rc = L.entmax_attn_fwd(fake, fake, fake, ctypes.byref(bad), 0, 1.5, 0, 3, 0.0,
+                           fake, fake, fake, fake, fake, fake, fake, 1 << 30, None)
+    assert rc == _lib.ENTMAX_ERR_INVALID_ARG
+    s3 = _lib.Shape(1, 1, 256, 48, 256 * 48, 256 * 48, 48)    # d=48 has no kernel
+    assert L.entmax_attn_impl_for(ctypes.byref(s3), 0) == -1
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    import paper_2502_12082_b200 as P
+    x = torch.zeros(1, 1, 128, 64, dtype=torch.bfloat16)
+    with pytest.raises(RuntimeError):
+        P.entmax_attn_fwd(x, x, x)
