@@ -2,16 +2,13 @@
 #include "entmax_attn.h"
 #include "runtime.h"
 #include "sm100_kernels.cuh"
+#include "sm100_tau.cuh"
 #include "tmap.h"
 
 namespace entmax {
 namespace sm100 {
 namespace {
 
-template <int D>
-constexpr size_t tau_smem(int Tc) {
-  return 1024 + Cfg<D>::TILE + ((D == 64) ? 4 : 3) * Cfg<D>::TILE + (size_t)Tc;
-}
 template <int D>
 constexpr size_t out_smem(int Tc) {
   return 1024 + Cfg<D>::TILE + ((D == 64) ? 3 : 2) * 2 * Cfg<D>::TILE + 65536 + (size_t)Tc;
@@ -50,10 +47,10 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}})) return rc;
   const dim3 grid(g.Tr, g.B * g.H);
   {
-    const size_t sm = tau_smem<D>(g.Tc);
+    const size_t sm = TauSmem<D>::bytes(g.Tc);
     if (int rc = set_smem(tau_kernel<D, E>, sm)) return rc;
     ProfScope ps("tau_sm100", st);
-    tau_kernel<D, E><<<grid, kThreads, sm, st>>>(tq, tk, g, ap, n_iter, tau, cand_cnt, cand_idx);
+    tau_kernel<D, E><<<grid, kTauThreads, sm, st>>>(tq, tk, g, ap, n_iter, tau, cand_cnt, cand_idx);
   }
   if (int rc = cuda_status("tau_sm100")) return rc;
   const size_t sm = out_smem<D>(g.Tc);

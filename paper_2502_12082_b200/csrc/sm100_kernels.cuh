@@ -114,152 +114,6 @@ __device__ __forceinline__ int compact_flags(const uint8_t* flags, int n, int32_
 }
 
 // =====================================================================================
-// K1: τ by Halley-bisection (Alg. 3 with Alg. 1 per row), candidate-block list.
-//   pass 0      : row max over visible keys (Alg. 1 lines 4-6)
-//   pass 1..T   : f, f', f'' sums at the current τ (Eqs. 3, 6, 7; Eq. 8 block additivity),
-//                 then one Alg. 1 update per row.  Pass T also flags every key block that has
-//                 some (row, key) with z > τ_lo (bracket entering pass T): a sound superset of
-//                 the final mask because τ_T >= τ_lo and fma(c', s, −τ) is monotone in τ.
-// =====================================================================================
-template <int D, int E>
-__global__ void __launch_bounds__(kThreads, 1)
-tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, Geom g, AlphaParams ap,
-           int n_iter, float* __restrict__ tau_out, int32_t* __restrict__ cand_cnt, int32_t* __restrict__ cand_idx) {
-  using C = Cfg<D>;
-  constexpr int NST = (D == 64) ? 4 : 3;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + C::TILE;
-  uint8_t* cflag = sK + NST * C::TILE;   // [Tc]
-  __shared__ __align__(8) uint64_t bar_q, k_full[NST], k_empty[NST], s_full[2], s_empty[2];
-  __shared__ uint32_t tmem_base_sh;
-
-  const int i = blockIdx.x, bh = blockIdx.y;
-  const int b = bh / g.H, h = bh - b * g.H;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = g.visible_kblocks(i);
-  const int nsteps = (1 + n_iter) * nkb;
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(&bar_q, 1);
-    for (int s = 0; s < NST; ++s) {
-      ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&k_empty[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_empty[s], 4);
-    }
-    ptx::fence_mbar_init();
-  }
-  for (int j = threadIdx.x; j < g.Tc; j += blockDim.x) cflag[j] = 0;
-  if (warp == 5) ptx::tmem_alloc<256>(&tmem_base_sh);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-
-  if (warp == 4) {
-    // ------------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      ptx::tma_prefetch_desc(&tq);
-      ptx::tma_prefetch_desc(&tk);
-      ptx::mbar_arrive_expect_tx(&bar_q, C::TILE);
-      tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
-      for (int k = 0; k < nsteps; ++k) {
-        const int j = k % nkb, st = k % NST;
-        ptx::mbar_wait(&k_empty[st], ((k / NST) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&k_full[st], C::TILE);
-        tma_tile<D>(sK + st * C::TILE, &tk, &k_full[st], j * kBc, h, b);
-      }
-    }
-  } else if (warp == 5) {
-    // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      ptx::mbar_wait(&bar_q, 0);
-      for (int k = 0; k < nsteps; ++k) {
-        const int st = k % NST, sb = k & 1;
-        ptx::mbar_wait(&k_full[st], (k / NST) & 1);
-        ptx::mbar_wait(&s_empty[sb], ((k >> 1) & 1) ^ 1);
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(tmem + sb * 128, sQ, sK + st * C::TILE, false);
-        ptx::mma_commit(&k_empty[st]);
-        ptx::mma_commit(&s_full[sb]);
-      }
-    }
-  } else {
-    // ------------------------------------------------------------------ math warps
-    const int row = i * kBr + threadIdx.x;
-    const bool valid = row < g.N;
-    const int my_last = g.causal ? row : g.N - 1;
-    const int cta_last = g.causal ? i * kBr : g.N - 1;   // every row of the CTA sees keys <= cta_last
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-    float smax = -INFINITY;
-    RowState rs{0.f, 0.f, 0.f};
-    int k = 0;
-    for (int pass = 0; pass <= n_iter; ++pass) {
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-      const bool last = pass == n_iter;
-      const float lo_in = rs.lo;
-      for (int j = 0; j < nkb; ++j, ++k) {
-        const int sb = k & 1;
-        ptx::mbar_wait(&s_full[sb], (k >> 1) & 1);
-        ptx::tc_fence_after();
-        const bool masked = (j + 1) * kBc - 1 > cta_last;
-        float bmax = -INFINITY;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          float s[32];
-          ld_chunk(lane_base + sb * 128 + c * 32, s);
-          if (masked) {
-            const int key0 = j * kBc + c * 32;
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (key0 + e > my_last) s[e] = -INFINITY;
-          }
-          float cm = s[0];
-#pragma unroll
-          for (int e = 1; e < 32; ++e) cm = fmaxf(cm, s[e]);
-          if (pass == 0) {
-            smax = fmaxf(smax, cm);
-          } else {
-            bmax = fmaxf(bmax, cm);
-            const bool hit = fmaf(cm, ap.cp, -rs.tau) > 0.f;
-            if (__any_sync(0xffffffffu, hit)) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) accum_f<E>(fmaf(s[e], ap.cp, -rs.tau), ap, a0, a1, a2);
-            }
-          }
-        }
-        ptx::tc_fence_before();
-        warp_arrive(&s_empty[sb]);
-        if (last) {
-          const bool f = valid && fmaf(bmax, ap.cp, -lo_in) > 0.f;
-          if (__any_sync(0xffffffffu, f) && lane == 0) cflag[j] = 1;
-        }
-      }
-      if (pass == 0) {
-        const float n_vis = g.causal ? (float)(row + 1) : (float)g.N;
-        rs = bracket_init(smax * ap.cp, n_vis, ap.alpha);
-      } else {
-        alg1_update(rs, a0, a1, a2, ap);
-      }
-    }
-    if (valid) tau_out[(long long)bh * g.N + row] = rs.tau;
-    ptx::named_bar_sync(1, kMathThreads);
-    if (warp == 0) {
-      const long long li = (long long)bh * g.Tr + i;
-      const int cnt = compact_flags(cflag, nkb, cand_idx + li * g.Tc);
-      if (lane == 0) cand_cnt[li] = cnt;
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 5) ptx::tmem_dealloc<256>(tmem);
-}
-
-// =====================================================================================
 // K2: output pass (Alg. 2 over the candidate blocks): S → P = [x]_+^e, U = [x]_+^{e−1};
 // O += P·V_j, O2 += U·V_j (TRAIN); exact M_ij = any(x > 0); mask row and 𝒬_i table.
 // =====================================================================================

@@ -30,7 +30,25 @@ probe_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUt
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base;
 
-  if (mode == 0) {
+  if (mode == 2) {
+    // thread r writes row r of A (K bf16 = K/2 packed columns) into TMEM columns 256 + [0, K/2)
+    const int r = threadIdx.x;
+    for (int c0 = 0; c0 < K / 2; c0 += 16) {
+      uint32_t w[16];
+      for (int e = 0; e < 16; ++e) {
+        const __nv_bfloat16* src = P + r * K + (c0 + e) * 2;
+        w[e] = ptx::pack_bf16(__bfloat162float(src[0]), __bfloat162float(src[1]));
+      }
+      ptx::tmem_st16(tmem + ((uint32_t)(warp * 32) << 16) + 256 + c0, w);
+    }
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    if (threadIdx.x == 0) {
+      const int chunks = K / 64;
+      ptx::mbar_arrive_expect_tx(&bar_tma, chunks * 16384);
+      for (int c = 0; c < chunks; ++c) ptx::tma_load_4d(sb + c * 16384, &tb, &bar_tma, c * 64, 0, 0, 0);
+    }
+  } else if (mode == 0) {
     if (threadIdx.x == 0) {
       const int chunks = K / 64;
       ptx::mbar_arrive_expect_tx(&bar_tma, chunks * 2 * 16384);
@@ -60,7 +78,13 @@ probe_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUt
   if (threadIdx.x == 0) {
     ptx::mbar_wait(&bar_tma, 0);
     ptx::tc_fence_after();
-    if (mode == 0) {
+    if (mode == 2) {
+      const uint32_t idesc = ptx::idesc_bf16(128, 128, 0, 0);
+      for (int ks = 0; ks < K / 16; ++ks) {
+        const uint32_t off = (ks / 4) * 16384 + (ks % 4) * 32;
+        ptx::mma_bf16_ts(tmem, tmem + 256 + ks * 8, ptx::sdesc_kmajor(ptx::smem_u32(sb) + off), idesc, ks > 0);
+      }
+    } else if (mode == 0) {
       const uint32_t idesc = ptx::idesc_bf16(128, 128, 0, 0);
       for (int ks = 0; ks < K / 16; ++ks) {
         const uint32_t off = (ks / 4) * 16384 + (ks % 4) * 32;
@@ -81,7 +105,7 @@ probe_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUt
   __syncwarp();
   ptx::mbar_wait(&bar_mma, 0);
   ptx::tc_fence_after();
-  const int ncols = (mode == 0) ? 128 : Nd;
+  const int ncols = (mode != 1) ? 128 : Nd;
   const int row = warp * 32 + (threadIdx.x & 31);
   for (int c0 = 0; c0 < ncols; c0 += 32) {
     uint32_t v[32];
@@ -96,8 +120,9 @@ probe_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUt
 
 extern "C" int probe_run(int mode, const void* A, const void* B, const void* P, float* D, int K, int Nd) {
   CUtensorMap ta, tb;
-  if (mode == 0) {
-    if (!make_tmap_bhnd(&ta, A, 1, 1, 128, K, 128LL * K, 128LL * K, K)) return 10;
+  if (mode == 0 || mode == 2) {
+    if (mode == 0 && !make_tmap_bhnd(&ta, A, 1, 1, 128, K, 128LL * K, 128LL * K, K)) return 10;
+    if (mode == 2) ta = CUtensorMap{};
     if (!make_tmap_bhnd(&tb, B, 1, 1, 128, K, 128LL * K, 128LL * K, K)) return 11;
   } else {
     ta = CUtensorMap{};

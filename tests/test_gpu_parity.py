@@ -96,3 +96,19 @@ def test_deterministic_and_head_sharding_bitwise():
         assert torch.equal(fw2.mask, fw.mask[sl])
         for a, b in zip(g2, grads):
             assert torch.equal(a, b[sl])
+
+
+@pytest.mark.parametrize("N,alpha,sigma2,causal", [
+    (512, 1.5, 0.05, False),    # near-uniform rows: every key is a τ candidate → list overflow path
+    (640, 1.5, 0.05, True),
+    (4096, 1.25, 6.0, False),   # small α: wide candidate set
+])
+def test_parity_candidate_overflow_fallback(N, alpha, sigma2, causal):
+    """Rows whose candidate list (z > τ_lo) overflows shared memory take the streaming Alg. 3
+    fallback inside the τ kernel; results must be identical in quality."""
+    _require_gpu()
+    spec = synth.HeadSpec("gaussian", sigma2_q=sigma2)
+    dev, ref = make_case(1, 2, N, 64, torch.bfloat16, seed=9, spec=spec)
+    fw, grads = run_gpu(dev, alpha, causal, 3)
+    for bh in range(2):
+        check_head(fw, ref, bh, alpha, causal, 3, torch.bfloat16, grads=grads)

@@ -41,3 +41,15 @@ def test_ss_mma_thread_written_a_mnmajor_b(Nd):
     assert L.probe_run(1, None, V.data_ptr(), P.data_ptr(), D.data_ptr(), 0, Nd) == 0
     ref = P.float() @ V.float()
     torch.testing.assert_close(D, ref, atol=1e-3, rtol=1e-4)
+
+
+@pytest.mark.parametrize("K", [64, 128])
+def test_ts_mma_a_in_tmem(K):
+    """A operand written to TMEM by threads (tcgen05.st, bf16 pairs per 32-bit column)."""
+    L = _lib()
+    g = torch.Generator().manual_seed(100 + K)
+    A = torch.randn(128, K, generator=g).to(torch.bfloat16).cuda()
+    B = torch.randn(128, K, generator=g).to(torch.bfloat16).cuda()
+    D = torch.empty(128, 128, dtype=torch.float32, device="cuda")
+    assert L.probe_run(2, None, B.data_ptr(), A.data_ptr(), D.data_ptr(), K, 0) == 0
+    torch.testing.assert_close(D, A.float() @ B.float().T, atol=1e-3, rtol=1e-4)
