@@ -24,7 +24,7 @@ namespace sm100 {
 
 constexpr int kTauThreads = 320;
 constexpr int kTauMath = 256;
-constexpr int kTauCap = 32;  // list slots per (row, column half)
+constexpr int kTauCap = 80;  // list slots per (row, column half); the count has a heavy tail
 constexpr int kTauSBuf = 4;  // S tiles in flight in TMEM (4 × 128 columns)
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -35,7 +35,7 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 
 template <int D>
 struct TauSmem {
-  static constexpr int NST = (D == 64) ? 8 : 4;   // K-tile ring depth (TMA latency ≈ several tiles)
+  static constexpr int NST = (D == 64) ? 4 : 2;   // K-tile ring depth
   static constexpr size_t tiles = (size_t)(1 + NST) * Cfg<D>::TILE;
   static constexpr size_t lists = (size_t)(kTauCap + 1) * kTauMath * (4 + 2);   // + scratch slot
   static constexpr size_t fixed = 1024 + tiles + lists + kTauMath * 4 * 4;  // + exchange scratch

@@ -151,3 +151,50 @@ extern "C" int ubench_run(int mode, int nst, int grid, int ntile, int kdim, cons
   cudaEventElapsedTime(ms, a, b);
   return e == cudaSuccess ? 0 : 100 + (int)e;
 }
+
+// TMEM → register read bandwidth: nwarp warps each repeatedly load 32 lanes × (x) columns.
+template <int X>
+__device__ __forceinline__ uint32_t tld(uint32_t taddr) {
+  uint32_t r[32];
+  if constexpr (X == 32) {
+    ptx::tmem_ld32(taddr, r);
+  } else {
+    uint32_t q[16];
+    ptx::tmem_ld16(taddr, q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) r[i] = q[i];
+#pragma unroll
+    for (int i = 16; i < 32; ++i) r[i] = 0;
+  }
+  ptx::tmem_wait_ld();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int i = 0; i < X; ++i) acc ^= r[i];
+  return acc;
+}
+
+template <int X>
+__global__ void __launch_bounds__(512, 1) tmem_rd(int iters, long long* cycles, uint32_t* sink) {
+  __shared__ uint32_t tbase;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) ptx::tmem_alloc<512>(&tbase);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tm = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  uint32_t acc = 0;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) acc += tld<X>(tm + ((it * X + warp * 64) & 511));
+  const long long t1 = clock64();
+  if ((threadIdx.x & 31) == 0) cycles[blockIdx.x * 16 + warp] = t1 - t0;
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc<512>(tbase);
+}
+
+extern "C" int tmem_rd_run(int x, int nwarps, int iters, long long* cycles, uint32_t* sink) {
+  if (x == 32) tmem_rd<32><<<148, nwarps * 32>>>(iters, cycles, sink);
+  else tmem_rd<16><<<148, nwarps * 32>>>(iters, cycles, sink);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
