@@ -3,6 +3,7 @@
 #include "runtime.h"
 #include "sm100_kernels.cuh"
 #include "sm100_tau.cuh"
+#include "sm100_fb.cuh"
 #include "tmap.h"
 
 namespace entmax {
@@ -11,15 +12,15 @@ namespace {
 
 template <int D>
 constexpr size_t out_smem(int Tc) {
-  return 1024 + Cfg<D>::TILE + ((D == 64) ? 3 : 2) * 2 * Cfg<D>::TILE + 65536 + (size_t)Tc;
+  return 1024 + Cfg<D>::TILE + ((D == 64) ? 4 : 2) * 2 * Cfg<D>::TILE + kFbMath * 4 + (size_t)Tc;
 }
 template <int D>
 constexpr size_t dkdv_smem() {
-  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 2 : 1) * (2 * Cfg<D>::TILE + 1024) + 65536;
+  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 3 : 2) * (2 * Cfg<D>::TILE + 1024);
 }
 template <int D>
 constexpr size_t dq_smem() {
-  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 2 : 1) * 2 * Cfg<D>::TILE + 32768;
+  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 4 : 2) * 2 * Cfg<D>::TILE;
 }
 
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
@@ -57,12 +58,12 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
   if (o2 != nullptr) {
     if (int rc = set_smem(out_kernel<D, E, true>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    out_kernel<D, E, true><<<grid, kThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
+    out_kernel<D, E, true><<<grid, kFbThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
                                                        (__nv_bfloat16*)o, (float*)o2, mask, row_cnt, row_idx);
   } else {
     if (int rc = set_smem(out_kernel<D, E, false>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    out_kernel<D, E, false><<<grid, kThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
+    out_kernel<D, E, false><<<grid, kFbThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
                                                         (__nv_bfloat16*)o, nullptr, mask, row_cnt, row_idx);
   }
   return cuda_status("out_sm100");
@@ -78,7 +79,7 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
     const size_t sm = dkdv_smem<D>();
     if (int rc = set_smem(dkdv_kernel<D, E>, sm)) return rc;
     ProfScope ps("dkdv_sm100", st);
-    dkdv_kernel<D, E><<<dim3(g.Tc, g.B * g.H), kThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, col_cnt,
+    dkdv_kernel<D, E><<<dim3(g.Tc, g.B * g.H), kFbThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, col_cnt,
                                                                      col_idx, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
   }
   if (int rc = cuda_status("dkdv_sm100")) return rc;
@@ -86,7 +87,7 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
     const size_t sm = dq_smem<D>();
     if (int rc = set_smem(dq_kernel<D, E>, sm)) return rc;
     ProfScope ps("dq_sm100", st);
-    dq_kernel<D, E><<<dim3(g.Tr, g.B * g.H), kThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, row_cnt, row_idx,
+    dq_kernel<D, E><<<dim3(g.Tr, g.B * g.H), kFbThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, row_cnt, row_idx,
                                                                    (__nv_bfloat16*)dq);
   }
   return cuda_status("dq_sm100");

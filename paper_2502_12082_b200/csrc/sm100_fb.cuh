@@ -1,0 +1,576 @@
+// sm100_fb.cuh — output pass and backward kernels (sm_100a), TMEM-resident P / U / dS.
+//
+// All three kernels: one CTA per 128-row block of one head, 320 threads —
+//   warps 0-7 : math warps.  Warp w owns TMEM lanes 32·(w & 3) (one row per thread) and the
+//               column half wg = w >> 2 of every 128-column tile (keys wg·64 .. wg·64+63 in the
+//               output / dQ kernels, queries wg·64 .. in the dK/dV kernel);
+//   warp  8   : TMA producer (stage ring of operand tiles, mbarrier full/empty);
+//   warp  9   : MMA issuer + TMEM owner.
+// The math warps write the bf16 operand they produce (P, U, dS, Pᵀ, dSᵀ) straight into TMEM with
+// tcgen05.st (two bf16 per 32-bit column: lane = row, column = k/2), and the second GEMM of each
+// kernel is a TS-MMA (A from TMEM, B = a [128 × d] tile used MN-major).  Nothing round-trips
+// through shared memory, which keeps smem bandwidth for the SS-MMAs and the TMA stream.
+#pragma once
+
+#include "sm100_kernels.cuh"
+
+namespace entmax {
+namespace sm100 {
+
+constexpr int kFbThreads = 320;
+constexpr int kFbMath = 256;
+
+// D[tmem, 128 × D] (+)= A[tmem, 128 × 128 bf16] · B[smem, 128 rows × D, MN-major]
+template <int D, typename ACol>
+__device__ __forceinline__ void mma_tmem_x_tile(uint32_t d_tmem, ACol acol, const uint8_t* b, bool accumulate) {
+  constexpr uint32_t idesc = ptx::idesc_bf16(128, D, 0, 1);
+  const uint32_t sb = ptx::smem_u32(b);
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+    ptx::mma_bf16_ts(d_tmem, acol(ks), ptx::sdesc_mnmajor(sb + ks * 2048, kChunkBytes), idesc,
+                     (accumulate || ks > 0) ? 1u : 0u);
+}
+
+// 32 consecutive columns → 32 floats (no wait)
+__device__ __forceinline__ void ld32f_nowait(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  ptx::tmem_ld32(taddr, r);
+#pragma unroll
+  for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(r[e]);
+}
+
+// store HALF fp32 columns of one row (TMEM chunk loads) as bf16 × scale to global.  The TMEM loads
+// are warp-collective, so every lane loads; only lanes with do_store write.
+template <int HALF>
+__device__ __forceinline__ void store_row_bf16(uint32_t taddr, __nv_bfloat16* dst, float scale, bool zero,
+                                               bool do_store) {
+#pragma unroll 1
+  for (int c = 0; c < HALF / 32; ++c) {
+    float v[32];
+    if (!zero) {
+      ld_chunk(taddr + c * 32, v);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = 0.f;
+    }
+    if (!do_store) continue;
+    uint4* p = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      p[q] = make_uint4(ptx::pack_bf16(v[8 * q] * scale, v[8 * q + 1] * scale),
+                        ptx::pack_bf16(v[8 * q + 2] * scale, v[8 * q + 3] * scale),
+                        ptx::pack_bf16(v[8 * q + 4] * scale, v[8 * q + 5] * scale),
+                        ptx::pack_bf16(v[8 * q + 6] * scale, v[8 * q + 7] * scale));
+  }
+}
+
+// =====================================================================================
+// Output pass (Alg. 2 over the candidate blocks, App. B.3): S = Q K_jᵀ → x = c'·s − τ,
+// P = [x]_+^e, U = [x]_+^{e−1}; O += P V_j, O⁽²⁾ += U V_j (TRAIN); M_ij = any(x > 0).
+// TMEM: two S buffers [0,256) — after the math warps read a buffer they overwrite their own
+// 64 columns with P (cols wg·64 + [0,32)) and U (wg·64 + [32,64)) — O at 256, O⁽²⁾ at 256 + D.
+// The MMA issue order S(0) S(1) | PV(0) UV(0) S(2) | PV(1) UV(1) S(3) … keeps the tensor pipe on
+// the next tile while the math warps work on the current one; S(k+2) is issued after PV(k) in
+// program order, so the in-order tensor pipe never overwrites P(k) before it is consumed.
+// =====================================================================================
+template <int D, int E, bool TRAIN>
+__global__ void __launch_bounds__(kFbThreads, 1)
+out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+           const __grid_constant__ CUtensorMap tv, Geom g, AlphaParams ap, const float* __restrict__ tau,
+           const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx, __nv_bfloat16* __restrict__ o,
+           float* __restrict__ o2, uint8_t* __restrict__ mask, int32_t* __restrict__ row_cnt,
+           int32_t* __restrict__ row_idx) {
+  using C = Cfg<D>;
+  constexpr int NST = (D == 64) ? 4 : 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sKV = sQ + C::TILE;                  // NST × [K tile | V tile]
+  float* xch = reinterpret_cast<float*>(sKV + NST * 2 * C::TILE);   // [256]
+  uint8_t* aflag = reinterpret_cast<uint8_t*>(xch + kFbMath);       // [Tc]
+  __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_full;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int i = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / g.H, h = bh - b * g.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long li = (long long)bh * g.Tr + i;
+  const int ncand = cand_cnt[li];
+  const int32_t* list = cand_idx + li * g.Tc;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar_q, 1);
+    for (int s = 0; s < NST; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(&s_full[s], 1);
+      ptx::mbar_init(&p_full[s], 8);
+    }
+    ptx::mbar_init(&o_full, 1);
+    ptx::fence_mbar_init();
+  }
+  for (int j = threadIdx.x; j < g.Tc; j += blockDim.x) aflag[j] = 0;
+  if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t t_o = tmem + 256, t_o2 = tmem + 256 + D;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tq);
+      ptx::tma_prefetch_desc(&tk);
+      ptx::tma_prefetch_desc(&tv);
+      ptx::mbar_arrive_expect_tx(&bar_q, C::TILE);
+      tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
+      for (int k = 0; k < ncand; ++k) {
+        const int j = list[k], st = k % NST;
+        ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
+        tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], j * kBc, h, b);
+        tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], j * kBc, h, b);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      ptx::mbar_wait(&bar_q, 0);
+      auto issue_s = [&](int k) {
+        const int st = k % NST;
+        ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
+        ptx::tc_fence_after();
+        mma_rows_x_rows<D>(tmem + (k & 1) * 128, sQ, sKV + st * 2 * C::TILE, false);
+        ptx::mma_commit(&s_full[k & 1]);
+      };
+      if (ncand > 0) issue_s(0);
+      if (ncand > 1) issue_s(1);
+      for (int k = 0; k < ncand; ++k) {
+        const int st = k % NST, sb = k & 1;
+        ptx::mbar_wait(&p_full[sb], (k >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t buf = tmem + sb * 128;
+        const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
+        mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+        if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+        ptx::mma_commit(&kv_empty[st]);
+        if (k + 2 < ncand) issue_s(k + 2);
+      }
+      ptx::mma_commit(&o_full);
+    }
+  } else {
+    const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
+    const int row = i * kBr + r;
+    const bool valid = row < g.N;
+    const int my_last = g.causal ? row : g.N - 1;
+    const int cta_last = g.causal ? i * kBr : g.N - 1;
+    const float tr = valid ? tau[(long long)bh * g.N + row] : INFINITY;
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    float usum = 0.f;
+    for (int k = 0; k < ncand; ++k) {
+      const int j = list[k], sb = k & 1;
+      const bool masked = (j + 1) * kBc - 1 > cta_last;
+      const uint32_t col = lane_base + sb * 128 + wg * 64;
+      ptx::mbar_wait(&s_full[sb], (k >> 1) & 1);
+      ptx::tc_fence_after();
+      float s0[32], s1[32];
+      ld32f_nowait(col, s0);
+      ld32f_nowait(col + 32, s1);
+      ptx::tmem_wait_ld();
+      uint32_t pp[32], pu[32];
+      float xmax = -INFINITY;
+      const int key0 = j * kBc + wg * 64;
+#pragma unroll
+      for (int e = 0; e < 64; e += 2) {
+        float x0 = fmaf(e < 32 ? s0[e] : s1[e - 32], ap.cp, -tr);
+        float x1 = fmaf(e < 32 ? s0[e + 1] : s1[e - 31], ap.cp, -tr);
+        if (masked) {
+          if (key0 + e > my_last) x0 = -INFINITY;
+          if (key0 + e + 1 > my_last) x1 = -INFINITY;
+        }
+        xmax = fmaxf(xmax, fmaxf(x0, x1));
+        float p0, u0, p1, u1;
+        p_and_u<E>(x0, ap, p0, u0);
+        p_and_u<E>(x1, ap, p1, u1);
+        usum += u0 + u1;
+        pp[e >> 1] = ptx::pack_bf16(p0, p1);
+        pu[e >> 1] = ptx::pack_bf16(u0, u1);
+      }
+      ptx::tmem_st32(col, pp);
+      if (TRAIN) ptx::tmem_st32(col + 32, pu);
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      warp_arrive(&p_full[sb]);
+      if (__any_sync(0xffffffffu, xmax > 0.f) && lane == 0) aflag[j] = 1;
+    }
+    // epilogue: O and O⁽²⁾ = (Σ U V)/ΣU; each column half written by its warpgroup
+    xch[tid] = usum;
+    ptx::named_bar_sync(1, kFbMath);
+    const float inv = 1.0f / (xch[r] + xch[128 + r]);
+    if (ncand > 0) {
+      ptx::mbar_wait(&o_full, 0);
+      ptx::tc_fence_after();
+    }
+    store_row_bf16<D / 2>(lane_base + 256 + wg * (D / 2), o + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2),
+                          1.0f, ncand == 0, valid);
+    if (TRAIN) {
+#pragma unroll 1
+      for (int c = 0; c < D / 64; ++c) {
+        float v[32];
+        if (ncand > 0) {
+          ld_chunk(lane_base + 256 + D + wg * (D / 2) + c * 32, v);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0.f;
+        }
+        if (valid) {
+          float4* dst = reinterpret_cast<float4*>(o2 + ((long long)bh * g.N + row) * D + wg * (D / 2) + c * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            dst[q] = make_float4(v[4 * q] * inv, v[4 * q + 1] * inv, v[4 * q + 2] * inv, v[4 * q + 3] * inv);
+        }
+      }
+    }
+    ptx::named_bar_sync(1, kFbMath);
+    uint8_t* mrow = mask + li * g.Tc;
+    for (int j = tid; j < g.Tc; j += kFbMath) mrow[j] = aflag[j];
+    if (warp == 0) {
+      const int cnt = compact_flags(aflag, g.Tc, row_idx + li * g.Tc);
+      if (lane == 0) row_cnt[li] = cnt;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 9) ptx::tmem_dealloc<512>(tmem);
+}
+
+// =====================================================================================
+// dQ_i over 𝒬_i (Alg. 5): S = Q_i K_jᵀ, dP = dO_i V_jᵀ (SS-MMAs); dS = U ⊙ (dP − δ) written to
+// TMEM; dQ_i += dS K_j (TS-MMA); dQ scaled by c at the end (Eq. 1).
+// TMEM: S [0,128), dP [128,256), dS [256,320) (wg·32 + …), dQ [320, 320+D).
+// Issue order S,dP(k+1) | dQ(k): the next tile's scores are computed while the math warps form dS(k).
+// =====================================================================================
+template <int D, int E>
+__global__ void __launch_bounds__(kFbThreads, 1)
+dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+          const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
+          const float* __restrict__ tau, const float* __restrict__ delta, const int32_t* __restrict__ row_cnt,
+          const int32_t* __restrict__ row_idx, __nv_bfloat16* __restrict__ dq) {
+  using C = Cfg<D>;
+  constexpr int NST = (D == 64) ? 4 : 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sQ = smem;
+  uint8_t* sDO = sQ + C::TILE;
+  uint8_t* sKV = sDO + C::TILE;                 // NST × [K | V]
+  __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full, s_empty, ds_full, ds_empty, acc_full;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int i = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / g.H, h = bh - b * g.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long li = (long long)bh * g.Tr + i;
+  const int cnt = row_cnt[li];
+  const int32_t* list = row_idx + li * g.Tc;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar_q, 1);
+    for (int s = 0; s < NST; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    ptx::mbar_init(&s_full, 1);
+    ptx::mbar_init(&s_empty, 8);
+    ptx::mbar_init(&ds_full, 8);
+    ptx::mbar_init(&ds_empty, 1);
+    ptx::mbar_init(&acc_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_ds = tmem + 256, t_dq = tmem + 320;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tk);
+      ptx::tma_prefetch_desc(&tv);
+      ptx::mbar_arrive_expect_tx(&bar_q, 2 * C::TILE);
+      tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
+      tma_tile<D>(sDO, &tdo, &bar_q, i * kBr, h, b);
+      for (int k = 0; k < cnt; ++k) {
+        const int jb = list[k], st = k % NST;
+        ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
+        tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], jb * kBc, h, b);
+        tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], jb * kBc, h, b);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      ptx::mbar_wait(&bar_q, 0);
+      auto issue_sdp = [&](int k) {
+        const int st = k % NST;
+        const uint8_t* sK = sKV + st * 2 * C::TILE;
+        ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
+        ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
+        ptx::tc_fence_after();
+        mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
+        mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
+        ptx::mma_commit(&s_full);
+      };
+      if (cnt > 0) issue_sdp(0);
+      for (int k = 0; k < cnt; ++k) {
+        if (k + 1 < cnt) issue_sdp(k + 1);
+        const int st = k % NST;
+        ptx::mbar_wait(&ds_full, k & 1);
+        ptx::tc_fence_after();
+        mma_tmem_x_tile<D>(t_dq, [&](int ks) { return t_ds + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
+        ptx::mma_commit(&kv_empty[st]);
+        ptx::mma_commit(&ds_empty);
+      }
+      ptx::mma_commit(&acc_full);
+    }
+  } else {
+    const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
+    const int row = i * kBr + r;
+    const bool valid = row < g.N;
+    const int my_last = g.causal ? row : g.N - 1;
+    const int cta_last = g.causal ? i * kBr : g.N - 1;
+    const float tr = valid ? tau[(long long)bh * g.N + row] : INFINITY;
+    const float dl = valid ? delta[(long long)bh * g.N + row] : 0.f;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    for (int k = 0; k < cnt; ++k) {
+      const int jb = list[k];
+      const bool masked = (jb + 1) * kBc - 1 > cta_last;
+      const int key0 = jb * kBc + wg * 64;
+      ptx::mbar_wait(&s_full, k & 1);
+      ptx::tc_fence_after();
+      uint32_t pd[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        float s[32], dp[32];
+        ld32f_nowait(lane_base + t_s + wg * 64 + hh * 32, s);
+        ld32f_nowait(lane_base + t_dp + wg * 64 + hh * 32, dp);
+        ptx::tmem_wait_ld();
+        if (hh == 1) {
+          ptx::tc_fence_before();
+          warp_arrive(&s_empty);
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float x0 = fmaf(s[e], ap.cp, -tr), x1 = fmaf(s[e + 1], ap.cp, -tr);
+          if (masked) {
+            if (key0 + hh * 32 + e > my_last) x0 = -INFINITY;
+            if (key0 + hh * 32 + e + 1 > my_last) x1 = -INFINITY;
+          }
+          float p0, u0, p1, u1;
+          p_and_u<E>(x0, ap, p0, u0);
+          p_and_u<E>(x1, ap, p1, u1);
+          pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(u0 * (dp[e] - dl), u1 * (dp[e + 1] - dl));
+        }
+      }
+      ptx::mbar_wait(&ds_empty, (k & 1) ^ 1);   // dQ(k−1) has consumed the previous dS
+      ptx::tc_fence_after();
+      ptx::tmem_st32(lane_base + t_ds + wg * 32, pd);
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      warp_arrive(&ds_full);
+    }
+    if (cnt > 0) {
+      ptx::mbar_wait(&acc_full, 0);
+      ptx::tc_fence_after();
+    }
+    store_row_bf16<D / 2>(lane_base + t_dq + wg * (D / 2), dq + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2),
+                          ap.scale, cnt == 0, valid);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 9) ptx::tmem_dealloc<512>(tmem);
+}
+
+// =====================================================================================
+// dK_j, dV_j over 𝒦_j (Alg. 4).  TMEM lanes = the 128 keys of block j.
+//   Sᵀ = K_j Q_iᵀ, dPᵀ = V_j dO_iᵀ (SS); Pᵀ and dSᵀ = Uᵀ ⊙ (dPᵀ − δ_i) to TMEM;
+//   dV_j += Pᵀ dO_i, dK_j += dSᵀ Q_i (TS); dK scaled by c at the end (Eq. 1).
+// d = 64: Sᵀ [0,128) dPᵀ [128,256) Pᵀ [256,320) dSᵀ [320,384) dV [384,448) dK [448,512), so the
+//         next step's Sᵀ/dPᵀ overlap this step's math.
+// d = 128: Pᵀ/dSᵀ overwrite each warpgroup's own Sᵀ/dPᵀ columns (dV [256,384), dK [384,512)).
+// =====================================================================================
+template <int D, int E>
+__global__ void __launch_bounds__(kFbThreads, 1)
+dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+            const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
+            const float* __restrict__ tau, const float* __restrict__ delta, const int32_t* __restrict__ col_cnt,
+            const int32_t* __restrict__ col_idx, __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv) {
+  using C = Cfg<D>;
+  constexpr bool ALIAS = (D == 128);
+  constexpr int NST = (D == 64) ? 3 : 2;
+  constexpr uint32_t STAGE = 2 * C::TILE + 1024;   // Q_i | dO_i | τ_i[128] | δ_i[128]
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::TILE;
+  uint8_t* sStage = sV + C::TILE;
+  __shared__ __align__(8) uint64_t bar_kv, qd_full[NST], qd_empty[NST], s_full, s_empty, p_full, p_empty, acc_full;
+  __shared__ uint32_t tmem_base_sh;
+
+  const int j = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / g.H, h = bh - b * g.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long lj = (long long)bh * g.Tc + j;
+  const int cnt = col_cnt[lj];
+  const int32_t* list = col_idx + lj * g.Tr;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar_kv, 1);
+    for (int s = 0; s < NST; ++s) {
+      ptx::mbar_init(&qd_full[s], 1);
+      ptx::mbar_init(&qd_empty[s], 1);
+    }
+    ptx::mbar_init(&s_full, 1);
+    ptx::mbar_init(&s_empty, 8);
+    ptx::mbar_init(&p_full, 8);
+    ptx::mbar_init(&p_empty, 1);
+    ptx::mbar_init(&acc_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const uint32_t t_s = tmem, t_dp = tmem + 128;
+  const uint32_t t_dv = tmem + (ALIAS ? 256 : 384), t_dk = t_dv + D;
+  auto pt_col = [&](int ks) { return ALIAS ? t_s + 8 * ks + (ks >= 4 ? 32 : 0) : tmem + 256 + 8 * ks; };
+  auto dst_col = [&](int ks) { return ALIAS ? t_dp + 8 * ks + (ks >= 4 ? 32 : 0) : tmem + 320 + 8 * ks; };
+
+  if (warp == 8) {
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tq);
+      ptx::tma_prefetch_desc(&tdo);
+      ptx::mbar_arrive_expect_tx(&bar_kv, 2 * C::TILE);
+      tma_tile<D>(sK, &tk, &bar_kv, j * kBc, h, b);
+      tma_tile<D>(sV, &tv, &bar_kv, j * kBc, h, b);
+    }
+    for (int k = 0; k < cnt; ++k) {
+      const int ib = list[k], st = k % NST;
+      uint8_t* stg = sStage + st * STAGE;
+      ptx::mbar_wait(&qd_empty[st], ((k / NST) & 1) ^ 1);
+      float* tq_s = reinterpret_cast<float*>(stg + 2 * C::TILE);
+      float* dl_s = tq_s + 128;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int rr = ib * kBr + lane * 4 + e;
+        tq_s[lane * 4 + e] = rr < g.N ? tau[(long long)bh * g.N + rr] : INFINITY;
+        dl_s[lane * 4 + e] = rr < g.N ? delta[(long long)bh * g.N + rr] : 0.f;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * C::TILE);
+        tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
+        tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      ptx::mbar_wait(&bar_kv, 0);
+      auto issue_sdp = [&](int k) {
+        const int st = k % NST;
+        const uint8_t* stg = sStage + st * STAGE;
+        ptx::mbar_wait(&qd_full[st], (k / NST) & 1);
+        if (!ALIAS) ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
+        ptx::tc_fence_after();
+        mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
+        mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
+        ptx::mma_commit(&s_full);
+      };
+      if (cnt > 0) issue_sdp(0);
+      for (int k = 0; k < cnt; ++k) {
+        if (!ALIAS && k + 1 < cnt) issue_sdp(k + 1);
+        const int st = k % NST;
+        const uint8_t* stg = sStage + st * STAGE;
+        ptx::mbar_wait(&p_full, k & 1);
+        ptx::tc_fence_after();
+        mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
+        mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
+        ptx::mma_commit(&qd_empty[st]);
+        ptx::mma_commit(&p_empty);
+        if (ALIAS && k + 1 < cnt) issue_sdp(k + 1);
+      }
+      ptx::mma_commit(&acc_full);
+    }
+  } else {
+    const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
+    const int key = j * kBc + r;
+    const bool valid = key < g.N;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    for (int k = 0; k < cnt; ++k) {
+      const int ib = list[k], st = k % NST;
+      const uint8_t* stg = sStage + st * STAGE;
+      const float4* tq4 = reinterpret_cast<const float4*>(stg + 2 * C::TILE) + wg * 16;
+      const float4* dl4 = tq4 + 32;
+      const bool diag = g.causal && ib == j;   // queries below the key inside the diagonal block
+      ptx::mbar_wait(&qd_full[st], (k / NST) & 1);   // τ_i, δ_i staged by the producer warp
+      ptx::mbar_wait(&s_full, k & 1);
+      ptx::tc_fence_after();
+      uint32_t pp[32], pd[32];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        float s[32], dp[32];
+        ld32f_nowait(lane_base + t_s + wg * 64 + hh * 32, s);
+        ld32f_nowait(lane_base + t_dp + wg * 64 + hh * 32, dp);
+        ptx::tmem_wait_ld();
+        if (!ALIAS && hh == 1) {
+          ptx::tc_fence_before();
+          warp_arrive(&s_empty);
+        }
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4) {
+          const float4 t4 = tq4[hh * 8 + q4], d4 = dl4[hh * 8 + q4];
+          const float tv4[4] = {t4.x, t4.y, t4.z, t4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pv[4], dsv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int ql = wg * 64 + hh * 32 + q4 * 4 + e;
+            float x = fmaf(s[q4 * 4 + e], ap.cp, -tv4[e]);
+            if (!valid || (diag && ql < r)) x = -INFINITY;
+            float u;
+            p_and_u<E>(x, ap, pv[e], u);
+            dsv[e] = u * (dp[q4 * 4 + e] - dv4[e]);
+          }
+          pp[hh * 16 + q4 * 2] = ptx::pack_bf16(pv[0], pv[1]);
+          pp[hh * 16 + q4 * 2 + 1] = ptx::pack_bf16(pv[2], pv[3]);
+          pd[hh * 16 + q4 * 2] = ptx::pack_bf16(dsv[0], dsv[1]);
+          pd[hh * 16 + q4 * 2 + 1] = ptx::pack_bf16(dsv[2], dsv[3]);
+        }
+      }
+      if (!ALIAS) {
+        ptx::mbar_wait(&p_empty, (k & 1) ^ 1);   // dV/dK(k−1) have consumed the previous Pᵀ, dSᵀ
+        ptx::tc_fence_after();
+      }
+      ptx::tmem_st32(lane_base + pt_col(wg * 4), pp);
+      ptx::tmem_st32(lane_base + dst_col(wg * 4), pd);
+      ptx::tmem_wait_st();
+      ptx::tc_fence_before();
+      warp_arrive(&p_full);
+    }
+    if (cnt > 0) {
+      ptx::mbar_wait(&acc_full, 0);
+      ptx::tc_fence_after();
+    }
+    const long long off = g.head_off(bh) + (long long)(valid ? key : 0) * g.sn + wg * (D / 2);
+    store_row_bf16<D / 2>(lane_base + t_dv + wg * (D / 2), dv + off, 1.0f, cnt == 0, valid);
+    store_row_bf16<D / 2>(lane_base + t_dk + wg * (D / 2), dk + off, ap.scale, cnt == 0, valid);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 9) ptx::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace sm100
+}  // namespace entmax
