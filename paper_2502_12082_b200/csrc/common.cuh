@@ -107,6 +107,47 @@ __device__ __forceinline__ void p_and_u(float x, const AlphaParams& ap, float& p
   }
 }
 
+// ---- packed f32x2 arithmetic (sm_100a FFMA2 / FMUL2 / FADD2): two lanes of work per issue slot
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\tmov.b64 rc, {%6,%7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\tmul.rn.f32x2 rd, ra, rb;\n\t"
+      "mov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\tadd.rn.f32x2 rd, ra, rb;\n\t"
+      "mov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// P and U for a pair of x values (same semantics as p_and_u), FMA-pipe friendly for E = 1, 2.
+template <int E>
+__device__ __forceinline__ void p_and_u2(float2 x, const AlphaParams& ap, float2& p, float2& u) {
+  if (E == 2) {
+    u = make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f));
+    p = fmul2(u, u);
+  } else if (E == 1) {
+    p = make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f));
+    u = make_float2(x.x > 0.f ? 1.f : 0.f, x.y > 0.f ? 1.f : 0.f);
+  } else {
+    p_and_u<E>(x.x, ap, p.x, u.x);
+    p_and_u<E>(x.y, ap, p.y, u.y);
+  }
+}
+
 // Alg. 1 state of one row.
 struct RowState {
   float lo, hi, tau;

@@ -12,6 +12,8 @@
 // through shared memory, which keeps smem bandwidth for the SS-MMAs and the TMA stream.
 #pragma once
 
+#include <type_traits>
+
 #include "sm100_kernels.cuh"
 
 namespace entmax {
@@ -29,6 +31,14 @@ __device__ __forceinline__ void mma_tmem_x_tile(uint32_t d_tmem, ACol acol, cons
   for (int ks = 0; ks < 8; ++ks)
     ptx::mma_bf16_ts(d_tmem, acol(ks), ptx::sdesc_mnmajor(sb + ks * 2048, kChunkBytes), idesc,
                      (accumulate || ks > 0) ? 1u : 0u);
+}
+
+__device__ __forceinline__ float4 ld_shared_f4(uint32_t addr_base_plus_idx16) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr_base_plus_idx16));
+  return v;
 }
 
 // 32 consecutive columns → 32 floats (no wait)
@@ -179,24 +189,29 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ld32f_nowait(col + 32, s1);
       ptx::tmem_wait_ld();
       uint32_t pp[32], pu[32];
+      float2 su = make_float2(0.f, 0.f);     // Σ U of this step (> 0 ⟺ some x > 0 for E ∈ {1, 2})
       float xmax = -INFINITY;
+      const float2 cp2 = make_float2(ap.cp, ap.cp), ntr2 = make_float2(-tr, -tr);
       const int key0 = j * kBc + wg * 64;
+      auto body = [&](auto masked_c) {
 #pragma unroll
-      for (int e = 0; e < 64; e += 2) {
-        float x0 = fmaf(e < 32 ? s0[e] : s1[e - 32], ap.cp, -tr);
-        float x1 = fmaf(e < 32 ? s0[e + 1] : s1[e - 31], ap.cp, -tr);
-        if (masked) {
-          if (key0 + e > my_last) x0 = -INFINITY;
-          if (key0 + e + 1 > my_last) x1 = -INFINITY;
+        for (int e = 0; e < 64; e += 2) {
+          float2 x = ffma2(make_float2(e < 32 ? s0[e] : s1[e - 32], e < 32 ? s0[e + 1] : s1[e - 31]), cp2, ntr2);
+          if constexpr (decltype(masked_c)::value) {
+            if (key0 + e > my_last) x.x = -INFINITY;
+            if (key0 + e + 1 > my_last) x.y = -INFINITY;
+          }
+          if (E != 1 && E != 2) xmax = fmaxf(xmax, fmaxf(x.x, x.y));
+          float2 p, u;
+          p_and_u2<E>(x, ap, p, u);
+          su = fadd2(su, u);
+          pp[e >> 1] = ptx::pack_bf16(p.x, p.y);
+          pu[e >> 1] = ptx::pack_bf16(u.x, u.y);
         }
-        xmax = fmaxf(xmax, fmaxf(x0, x1));
-        float p0, u0, p1, u1;
-        p_and_u<E>(x0, ap, p0, u0);
-        p_and_u<E>(x1, ap, p1, u1);
-        usum += u0 + u1;
-        pp[e >> 1] = ptx::pack_bf16(p0, p1);
-        pu[e >> 1] = ptx::pack_bf16(u0, u1);
-      }
+      };
+      if (masked) body(std::true_type{}); else body(std::false_type{});
+      usum += su.x + su.y;
+      if (E == 1 || E == 2) xmax = su.x + su.y;   // exact: every U > 0 iff x > 0 (no underflow for e <= 2)
       ptx::tmem_st32(col, pp);
       if (TRAIN) ptx::tmem_st32(col + 32, pu);
       ptx::tmem_wait_st();
@@ -350,6 +365,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       ptx::mbar_wait(&s_full, k & 1);
       ptx::tc_fence_after();
       uint32_t pd[32];
+      const float2 cp2 = make_float2(ap.cp, ap.cp), ntr2 = make_float2(-tr, -tr), ndl2 = make_float2(-dl, -dl);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         float s[32], dp[32];
@@ -360,18 +376,21 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
           ptx::tc_fence_before();
           warp_arrive(&s_empty);
         }
+        auto body = [&](auto masked_c) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float x0 = fmaf(s[e], ap.cp, -tr), x1 = fmaf(s[e + 1], ap.cp, -tr);
-          if (masked) {
-            if (key0 + hh * 32 + e > my_last) x0 = -INFINITY;
-            if (key0 + hh * 32 + e + 1 > my_last) x1 = -INFINITY;
+          for (int e = 0; e < 32; e += 2) {
+            float2 x = ffma2(make_float2(s[e], s[e + 1]), cp2, ntr2);
+            if constexpr (decltype(masked_c)::value) {
+              if (key0 + hh * 32 + e > my_last) x.x = -INFINITY;
+              if (key0 + hh * 32 + e + 1 > my_last) x.y = -INFINITY;
+            }
+            float2 p, u;
+            p_and_u2<E>(x, ap, p, u);
+            const float2 ds = fmul2(u, fadd2(make_float2(dp[e], dp[e + 1]), ndl2));
+            pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
           }
-          float p0, u0, p1, u1;
-          p_and_u<E>(x0, ap, p0, u0);
-          p_and_u<E>(x1, ap, p1, u1);
-          pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(u0 * (dp[e] - dl), u1 * (dp[e + 1] - dl));
-        }
+        };
+        if (masked) body(std::true_type{}); else body(std::false_type{});
       }
       ptx::mbar_wait(&ds_empty, (k & 1) ^ 1);   // dQ(k−1) has consumed the previous dS
       ptx::tc_fence_after();
@@ -512,8 +531,8 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
     for (int k = 0; k < cnt; ++k) {
       const int ib = list[k], st = k % NST;
       const uint8_t* stg = sStage + st * STAGE;
-      const float4* tq4 = reinterpret_cast<const float4*>(stg + 2 * C::TILE) + wg * 16;
-      const float4* dl4 = tq4 + 32;
+      const uint32_t tq4 = ptx::smem_u32(stg + 2 * C::TILE) + wg * 256;   // τ_i (float4 units below)
+      const uint32_t dl4 = tq4 + 512;                                      // δ_i
       const bool diag = g.causal && ib == j;   // queries below the key inside the diagonal block
       ptx::mbar_wait(&qd_full[st], (k / NST) & 1);   // τ_i, δ_i staged by the producer warp
       ptx::mbar_wait(&s_full, k & 1);
@@ -529,25 +548,29 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
           ptx::tc_fence_before();
           warp_arrive(&s_empty);
         }
+        auto body = [&](auto masked_c) {
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4) {
-          const float4 t4 = tq4[hh * 8 + q4], d4 = dl4[hh * 8 + q4];
-          const float tv4[4] = {t4.x, t4.y, t4.z, t4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
-          float pv[4], dsv[4];
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 t4 = ld_shared_f4(tq4 + (hh * 8 + q4) * 16), d4 = ld_shared_f4(dl4 + (hh * 8 + q4) * 16);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int ql = wg * 64 + hh * 32 + q4 * 4 + e;
-            float x = fmaf(s[q4 * 4 + e], ap.cp, -tv4[e]);
-            if (!valid || (diag && ql < r)) x = -INFINITY;
-            float u;
-            p_and_u<E>(x, ap, pv[e], u);
-            dsv[e] = u * (dp[q4 * 4 + e] - dv4[e]);
+            for (int e = 0; e < 4; e += 2) {
+              const float2 tq2 = e == 0 ? make_float2(-t4.x, -t4.y) : make_float2(-t4.z, -t4.w);
+              const float2 dq2 = e == 0 ? make_float2(-d4.x, -d4.y) : make_float2(-d4.z, -d4.w);
+              float2 x = ffma2(make_float2(s[q4 * 4 + e], s[q4 * 4 + e + 1]), make_float2(ap.cp, ap.cp), tq2);
+              if constexpr (decltype(masked_c)::value) {
+                const int ql = wg * 64 + hh * 32 + q4 * 4 + e;
+                if (!valid || (diag && ql < r)) x.x = -INFINITY;
+                if (!valid || (diag && ql + 1 < r)) x.y = -INFINITY;
+              }
+              float2 p, u;
+              p_and_u2<E>(x, ap, p, u);
+              const float2 ds = fmul2(u, fadd2(make_float2(dp[q4 * 4 + e], dp[q4 * 4 + e + 1]), dq2));
+              pp[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(p.x, p.y);
+              pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+            }
           }
-          pp[hh * 16 + q4 * 2] = ptx::pack_bf16(pv[0], pv[1]);
-          pp[hh * 16 + q4 * 2 + 1] = ptx::pack_bf16(pv[2], pv[3]);
-          pd[hh * 16 + q4 * 2] = ptx::pack_bf16(dsv[0], dsv[1]);
-          pd[hh * 16 + q4 * 2 + 1] = ptx::pack_bf16(dsv[2], dsv[3]);
-        }
+        };
+        if (!valid || diag) body(std::true_type{}); else body(std::false_type{});
       }
       if (!ALIAS) {
         ptx::mbar_wait(&p_empty, (k & 1) ^ 1);   // dV/dK(k−1) have consumed the previous Pᵀ, dSᵀ
