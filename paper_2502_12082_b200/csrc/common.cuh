@@ -165,6 +165,11 @@ __device__ __forceinline__ RowState bracket_init(float zmax, float n_visible, fl
 // One Alg. 1 iteration given the accumulated sums at the current τ (lines 8-14):
 // bracket update (Eq. 4, tie f = 0 → τ_lo = τ), Halley candidate (Eq. 5), accept iff it lies in
 // the updated bracket (inclusive) and is finite, else midpoint.
+// Finite-precision reading (DESIGN.md r5): a candidate within a few fp32 ulps outside the bracket is
+// accepted and clamped to it.  In exact arithmetic this is Alg. 1 itself; it matters when τ* sits on
+// the bracket end (e.g. a single-element support gives τ* = τ_lo = m − 1, which the Newton/Halley
+// step reaches exactly in real arithmetic but may overshoot by an ulp in fp32, which would otherwise
+// demote the row to linear bisection for every remaining iteration).
 __device__ __forceinline__ void alg1_update(RowState& s, float a0, float a1, float a2, const AlphaParams& ap) {
   float f = a0 - 1.0f;         // Eq. 3
   float f1 = ap.c1 * a1;       // Eq. 6
@@ -172,8 +177,9 @@ __device__ __forceinline__ void alg1_update(RowState& s, float a0, float a1, flo
   if (f < 0.f) s.hi = s.tau; else s.lo = s.tau;
   float den = 2.0f * f1 * f1 - f * f2;
   float th = s.tau - 2.0f * f * f1 / den;
-  bool ok = (den != 0.f) && isfinite(th) && th >= s.lo && th <= s.hi;
-  s.tau = ok ? th : 0.5f * (s.lo + s.hi);
+  const float slack = 8.0f * 1.1920929e-7f * fmaxf(fabsf(s.lo), fabsf(s.hi));   // 8 ulp
+  bool ok = (den != 0.f) && isfinite(th) && th >= s.lo - slack && th <= s.hi + slack;
+  s.tau = ok ? fminf(fmaxf(th, s.lo), s.hi) : 0.5f * (s.lo + s.hi);
 }
 
 template <typename T> __device__ __forceinline__ float to_f(T v);

@@ -39,7 +39,7 @@ struct TauSmem {
   static constexpr size_t tiles = (size_t)(1 + NST) * Cfg<D>::TILE;
   static constexpr size_t lists = (size_t)(kTauCap + 1) * kTauMath * (4 + 2);   // + scratch slot
   static constexpr size_t fixed = 1024 + tiles + lists + kTauMath * 4 * 4;  // + exchange scratch
-  static size_t bytes(int Tc) { return fixed + 3 * (size_t)Tc + 64; }
+  static size_t bytes(int Tc) { return fixed + 4 * (size_t)Tc + 64; }   // cflag, aflag (u8) + cblk (u16)
 };
 
 template <int D, int E>

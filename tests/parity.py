@@ -80,3 +80,68 @@ def run_gpu(dev_inputs, alpha, causal, n_iter, training=True):
     grads = P.entmax_attn_bwd(q, k, v, do, fw, alpha, causal) if training else None
     torch.cuda.synchronize()
     return fw, grads
+
+
+def check_head_sampled(res, ref_inputs, bh, alpha, causal, n_iter, dtype, row_blocks, key_blocks=(), grads=None,
+                       Br=128, Bc=128):
+    """Full-size check of one head on sampled outputs the oracle computes one by one:
+    τ, O, O⁽²⁾, the mask row and the 𝒬 table of whole query blocks `row_blocks`, dQ of those rows,
+    and dK/dV of whole key blocks `key_blocks` (their oracle sums need τ of every row that sees
+    them: all rows, or for causal attention only the rows at or after the block)."""
+    q, k, v, do = [x.reshape((-1,) + x.shape[-2:])[bh] for x in ref_inputs]
+    N, d = q.shape
+    tol = TOL[dtype]
+    rows = np.concatenate([np.arange(i * Br, min(N, (i + 1) * Br)) for i in row_blocks])
+    fw = O.attn_fwd(q, k, v, alpha, causal, n_iter, rows=rows)
+    tau_g = res.tau.reshape(-1, N)[bh].double().cpu().numpy()
+    err_tau = np.max(np.abs(tau_g[rows] - fw["tau"]) / np.maximum(1.0, np.abs(fw["tau"])))
+    assert err_tau <= TAU_RTOL, ("tau", err_tau)
+    o_g = res.o.reshape(-1, N, d)[bh].double().cpu().numpy()[rows]
+    assert np.abs(o_g - fw["O"]).max() <= tol["o"], ("O", np.abs(o_g - fw["O"]).max())
+    if res.o2 is not None:
+        o2_g = res.o2.reshape(-1, N, d)[bh].double().cpu().numpy()[rows]
+        assert np.abs(o2_g - fw["O2"]).max() <= tol["o"], ("O2", np.abs(o2_g - fw["O2"]).max())
+    tau_full = np.zeros(N)
+    tau_full[rows] = fw["tau"]
+    M_ref, margin = O.block_mask(q, k, tau_full, alpha, causal, row_blocks=row_blocks)
+    assert margin > MARGIN_MIN, ("block margin too small for a bit-exact mask check", margin)
+    Tc = M_ref.shape[1]
+    Tr = -(-N // Br)
+    M_g = res.mask.reshape(-1, Tr, Tc)[bh].cpu().numpy()[list(row_blocks)]
+    assert np.array_equal(M_g, M_ref), ("mask", np.argwhere(M_g != M_ref)[:10])
+    cnt = res.row_cnt.reshape(-1, Tr)[bh].cpu().numpy()
+    idx = res.row_idx.reshape(-1, Tr, Tc)[bh].cpu().numpy()
+    for a, i in enumerate(row_blocks):
+        js = np.nonzero(M_ref[a])[0]
+        assert cnt[i] == len(js) and np.array_equal(idx[i, :cnt[i]], js), ("row table", i)
+    out = dict(tau=err_tau, density=float(M_ref.mean()))
+    if grads is None:
+        return out
+    bw = O.attn_bwd(q, k, v, do, tau_full, alpha, causal, rows=rows)
+    dq_g = grads[0].reshape(-1, N, d)[bh].double().cpu().numpy()[rows]
+    out["dQ"] = rel_l2(dq_g, bw["dQ"][rows])
+    assert out["dQ"] <= tol["g"], ("dQ", out["dQ"])
+    if key_blocks:
+        keys = np.concatenate([np.arange(j * Bc, min(N, (j + 1) * Bc)) for j in key_blocks])
+        need = np.arange(keys.min(), N) if causal else np.arange(N)
+        tau_need = np.zeros(N)
+        tau_need[need] = O.solve_tau(q, k, alpha, causal, n_iter, rows=need)
+        bwk = O.attn_bwd(q, k, v, do, tau_need, alpha, causal, key_cols=keys, rows=need)
+        for name, g, ref in (("dK", grads[1], bwk["dK"]), ("dV", grads[2], bwk["dV"])):
+            gg = g.reshape(-1, N, d)[bh].double().cpu().numpy()[keys]
+            out[name] = rel_l2(gg, ref)
+            assert out[name] <= tol["g"], (name, out[name])
+    return out
+
+
+def check_grad_identities(grads, ref_inputs, bh, dtype, tol=3e-2):
+    """Size-independent properties of the backward (any N): Σ_j dV_j = Σ_i (Σ_j P_ij) dO_i ≈ Σ_i dO_i
+    (rows of P sum to 1 up to the τ accuracy) and Σ_j dK_j = c Σ_i (Σ_j dS_ij) Q_i ≈ 0 (each row of
+    dS = U ⊙ (dP − δ) sums to zero by the definition of δ)."""
+    do = ref_inputs[3].reshape((-1,) + ref_inputs[3].shape[-2:])[bh]
+    N, d = do.shape
+    dv = grads[2].reshape(-1, N, d)[bh].double().cpu().numpy()
+    dk = grads[1].reshape(-1, N, d)[bh].double().cpu().numpy()
+    sv, sd = dv.sum(0), do.sum(0)
+    assert np.linalg.norm(sv - sd) <= tol * np.linalg.norm(sd) + 1e-2 * np.sqrt(N), ("sum dV", sv[:4], sd[:4])
+    assert np.linalg.norm(dk.sum(0)) <= tol * np.abs(dk).sum(0).max(), ("sum dK", np.linalg.norm(dk.sum(0)))

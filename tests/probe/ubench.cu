@@ -64,6 +64,19 @@ ubench(const __grid_constant__ CUtensorMap tk, int mode, int ntile, int kdim, in
       ptx::mbar_wait(&done, 0);
       cycles[blockIdx.x] = clock64() - t0;
     }
+  } else if (mode == 20) {  // TMA only, [128 x 64] tile as two boxes of 64 interleaved rows ([N/2,128] view)
+    if (threadIdx.x == 0) {
+      for (int t = 0; t < ntile + NST; ++t) {
+        if (t >= NST) ptx::mbar_wait(&full[(t - NST) % NST], ((t - NST) / NST) & 1);
+        if (t < ntile) {
+          const int st = t % NST;
+          ptx::mbar_arrive_expect_tx(&full[st], 16384);
+          const int row = (((blockIdx.x * 7 + t) * 128) % nrows) / 2;
+          for (int c = 0; c < 2; ++c) ptx::tma_load_4d(sK + st * 16384 + c * 8192, &tk, &full[st], c * 64, row, 0, 0);
+        }
+      }
+      cycles[blockIdx.x] = clock64() - t0;
+    }
   } else if (mode >= 10) {  // TMA only, tile [128 x 64] split into nbox = mode-10 boxes of 128/nbox rows
     const int nbox = mode - 10, brow = 128 / nbox;
     if (threadIdx.x == 0) {
@@ -131,9 +144,13 @@ ubench(const __grid_constant__ CUtensorMap tk, int mode, int ntile, int kdim, in
 extern "C" int ubench_run(int mode, int nst, int grid, int ntile, int kdim, const void* K, int nrows, long long* cycles,
                           float* ms) {
   CUtensorMap tk;
-  const int box_rows = mode >= 10 ? 128 / (mode - 10) : 128;
-  if (!make_tmap_bhnd(&tk, K, 1, 1, nrows, kdim, (long long)nrows * kdim, (long long)nrows * kdim, kdim, box_rows))
-    return 10;
+  if (mode == 20) {
+    if (!make_tmap_bhnd(&tk, K, 1, 1, nrows / 2, 128, (long long)nrows * 64, (long long)nrows * 64, 128, 64)) return 10;
+  } else {
+    const int box_rows = mode >= 10 ? 128 / (mode - 10) : 128;
+    if (!make_tmap_bhnd(&tk, K, 1, 1, nrows, kdim, (long long)nrows * kdim, (long long)nrows * kdim, kdim, box_rows))
+      return 10;
+  }
   const int smem = 32768 + nst * 128 * kdim * 2 + 1024;
   cudaEvent_t a, b;
   cudaEventCreate(&a);
