@@ -9,7 +9,19 @@ LIB    := paper_2502_12082_b200/libentmax_attn.so
 
 PROBE  := tests/probe/libprobe.so
 
+TRACE  := tests/probe/libentmax_trace.so
+
 all: $(LIB) $(PROBE)
+
+trace: $(TRACE)
+
+trace-nold: tests/probe/libentmax_trace_nold.so
+
+tests/probe/libentmax_trace_nold.so: $(wildcard $(SRC)/*.cu $(SRC)/*.cuh $(SRC)/*.h) tests/probe/trace_api.cu
+	$(NVCC) $(ARCH) $(CFLAGS) -DENTMAX_TRACE -DENTMAX_TRACE_NOLD -rdc=true -shared -o $@ $(SRC)/entmax_attn.cu $(SRC)/simt.cu $(SRC)/sm100.cu tests/probe/trace_api.cu
+
+$(TRACE): $(wildcard $(SRC)/*.cu $(SRC)/*.cuh $(SRC)/*.h) tests/probe/trace_api.cu
+	$(NVCC) $(ARCH) $(CFLAGS) -DENTMAX_TRACE -rdc=true -shared -o $@ $(SRC)/entmax_attn.cu $(SRC)/simt.cu $(SRC)/sm100.cu tests/probe/trace_api.cu
 
 $(PROBE): tests/probe/probe.cu $(SRC)/sm100_ptx.cuh $(SRC)/tmap.h
 	$(NVCC) $(ARCH) $(CFLAGS) -shared -o $@ $<
@@ -25,4 +37,4 @@ clean:
 	rm -rf build $(LIB) $(PROBE)
 
 -include build/*.d
-.PHONY: all clean
+.PHONY: all clean trace

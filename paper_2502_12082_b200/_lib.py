@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libentmax_attn.so")
+# ENTMAX_ATTN_LIB: diagnostics only (e.g. the -DENTMAX_TRACE build under tests/probe)
+LIB_PATH = os.environ.get("ENTMAX_ATTN_LIB", os.path.join(_HERE, "libentmax_attn.so"))
 
 ENTMAX_OK, ENTMAX_ERR_INVALID_ARG, ENTMAX_ERR_UNSUPPORTED, ENTMAX_ERR_WORKSPACE, ENTMAX_ERR_CUDA = range(5)
 ENTMAX_BF16, ENTMAX_FP32 = 0, 1

@@ -44,14 +44,17 @@ template <int D, int E>
 int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const AlphaParams& ap, int n_iter, void* o,
           void* o2, float* tau, uint8_t* mask, int32_t* row_cnt, int32_t* row_idx, int32_t* cand_cnt,
           int32_t* cand_idx, cudaStream_t st) {
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, tk64;
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}})) return rc;
+  if (!make_tmap_bhnd(&tk64, k, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn, 64))
+    return fail(ENTMAX_ERR_INVALID_ARG, "cuTensorMapEncodeTiled failed (64-row K boxes)");
   const dim3 grid(g.Tr, g.B * g.H);
   {
     const size_t sm = TauSmem<D>::bytes(g.Tc);
     if (int rc = set_smem(tau_kernel<D, E>, sm)) return rc;
     ProfScope ps("tau_sm100", st);
-    tau_kernel<D, E><<<grid, kTauThreads, sm, st>>>(tq, tk, g, ap, n_iter, tau, cand_cnt, cand_idx);
+    tau_kernel<D, E><<<dim3((g.Tr + 1) & ~1, g.B * g.H), kTauThreads, sm, st>>>(tq, tk64, g, ap, n_iter, tau, cand_cnt,
+                                                                               cand_idx);
   }
   if (int rc = cuda_status("tau_sm100")) return rc;
   const size_t sm = out_smem<D>(g.Tc);

@@ -29,7 +29,7 @@ __device__ __forceinline__ void mma_tmem_x_tile(uint32_t d_tmem, ACol acol, cons
   const uint32_t sb = ptx::smem_u32(b);
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks)
-    ptx::mma_bf16_ts(d_tmem, acol(ks), ptx::sdesc_mnmajor(sb + ks * 2048, kChunkBytes), idesc,
+    ptx::mma_bf16_ts_elect(d_tmem, acol(ks), ptx::sdesc_mnmajor(sb + ks * 2048, kChunkBytes), idesc,
                      (accumulate || ks > 0) ? 1u : 0u);
 }
 
@@ -130,45 +130,41 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const uint32_t t_o = tmem + 256, t_o2 = tmem + 256 + D;
 
   if (warp == 8) {
-    if (lane == 0) {
-      ptx::tma_prefetch_desc(&tq);
-      ptx::tma_prefetch_desc(&tk);
-      ptx::tma_prefetch_desc(&tv);
-      ptx::mbar_arrive_expect_tx(&bar_q, C::TILE);
-      tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
-      for (int k = 0; k < ncand; ++k) {
-        const int j = list[k], st = k % NST;
-        ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
-        tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], j * kBc, h, b);
-        tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], j * kBc, h, b);
-      }
+    ptx::tma_prefetch_desc(&tq);
+    ptx::tma_prefetch_desc(&tk);
+    ptx::tma_prefetch_desc(&tv);
+    ptx::mbar_arrive_expect_tx_elect(&bar_q, C::TILE);
+    tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
+    for (int k = 0; k < ncand; ++k) {
+      const int j = list[k], st = k % NST;
+      ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+      ptx::mbar_arrive_expect_tx_elect(&kv_full[st], 2 * C::TILE);
+      tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], j * kBc, h, b);
+      tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], j * kBc, h, b);
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      ptx::mbar_wait(&bar_q, 0);
-      auto issue_s = [&](int k) {
-        const int st = k % NST;
-        ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(tmem + (k & 1) * 128, sQ, sKV + st * 2 * C::TILE, false);
-        ptx::mma_commit(&s_full[k & 1]);
-      };
-      if (ncand > 0) issue_s(0);
-      if (ncand > 1) issue_s(1);
-      for (int k = 0; k < ncand; ++k) {
-        const int st = k % NST, sb = k & 1;
-        ptx::mbar_wait(&p_full[sb], (k >> 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t buf = tmem + sb * 128;
-        const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
-        mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
-        if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
-        ptx::mma_commit(&kv_empty[st]);
-        if (k + 2 < ncand) issue_s(k + 2);
-      }
-      ptx::mma_commit(&o_full);
+    ptx::mbar_wait(&bar_q, 0);
+    auto issue_s = [&](int k) {
+      const int st = k % NST;
+      ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
+      ptx::tc_fence_after();
+      mma_rows_x_rows<D>(tmem + (k & 1) * 128, sQ, sKV + st * 2 * C::TILE, false);
+      ptx::mma_commit_elect(&s_full[k & 1]);
+    };
+    if (ncand > 0) issue_s(0);
+    if (ncand > 1) issue_s(1);
+    for (int k = 0; k < ncand; ++k) {
+      const int st = k % NST, sb = k & 1;
+      ptx::mbar_wait(&p_full[sb], (k >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t buf = tmem + sb * 128;
+      const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
+      mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+      if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+      ptx::mma_commit_elect(&kv_empty[st]);
+      if (k + 2 < ncand) issue_s(k + 2);
     }
+    ptx::mma_commit_elect(&o_full);
   } else {
     const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
     const int row = i * kBr + r;
@@ -310,45 +306,41 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_ds = tmem + 256, t_dq = tmem + 320;
 
   if (warp == 8) {
-    if (lane == 0) {
-      ptx::tma_prefetch_desc(&tk);
-      ptx::tma_prefetch_desc(&tv);
-      ptx::mbar_arrive_expect_tx(&bar_q, 2 * C::TILE);
-      tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
-      tma_tile<D>(sDO, &tdo, &bar_q, i * kBr, h, b);
-      for (int k = 0; k < cnt; ++k) {
-        const int jb = list[k], st = k % NST;
-        ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
-        tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], jb * kBc, h, b);
-        tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], jb * kBc, h, b);
-      }
+    ptx::tma_prefetch_desc(&tk);
+    ptx::tma_prefetch_desc(&tv);
+    ptx::mbar_arrive_expect_tx_elect(&bar_q, 2 * C::TILE);
+    tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
+    tma_tile<D>(sDO, &tdo, &bar_q, i * kBr, h, b);
+    for (int k = 0; k < cnt; ++k) {
+      const int jb = list[k], st = k % NST;
+      ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+      ptx::mbar_arrive_expect_tx_elect(&kv_full[st], 2 * C::TILE);
+      tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], jb * kBc, h, b);
+      tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], jb * kBc, h, b);
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      ptx::mbar_wait(&bar_q, 0);
-      auto issue_sdp = [&](int k) {
-        const int st = k % NST;
-        const uint8_t* sK = sKV + st * 2 * C::TILE;
-        ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
-        ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
-        mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
-        ptx::mma_commit(&s_full);
-      };
-      if (cnt > 0) issue_sdp(0);
-      for (int k = 0; k < cnt; ++k) {
-        if (k + 1 < cnt) issue_sdp(k + 1);
-        const int st = k % NST;
-        ptx::mbar_wait(&ds_full, k & 1);
-        ptx::tc_fence_after();
-        mma_tmem_x_tile<D>(t_dq, [&](int ks) { return t_ds + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
-        ptx::mma_commit(&kv_empty[st]);
-        ptx::mma_commit(&ds_empty);
-      }
-      ptx::mma_commit(&acc_full);
+    ptx::mbar_wait(&bar_q, 0);
+    auto issue_sdp = [&](int k) {
+      const int st = k % NST;
+      const uint8_t* sK = sKV + st * 2 * C::TILE;
+      ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
+      ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
+      ptx::tc_fence_after();
+      mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
+      mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
+      ptx::mma_commit_elect(&s_full);
+    };
+    if (cnt > 0) issue_sdp(0);
+    for (int k = 0; k < cnt; ++k) {
+      if (k + 1 < cnt) issue_sdp(k + 1);
+      const int st = k % NST;
+      ptx::mbar_wait(&ds_full, k & 1);
+      ptx::tc_fence_after();
+      mma_tmem_x_tile<D>(t_dq, [&](int ks) { return t_ds + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
+      ptx::mma_commit_elect(&kv_empty[st]);
+      ptx::mma_commit_elect(&ds_empty);
     }
+    ptx::mma_commit_elect(&acc_full);
   } else {
     const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
     const int row = i * kBr + r;
@@ -468,13 +460,11 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   auto dst_col = [&](int ks) { return ALIAS ? t_dp + 8 * ks + (ks >= 4 ? 32 : 0) : tmem + 320 + 8 * ks; };
 
   if (warp == 8) {
-    if (lane == 0) {
-      ptx::tma_prefetch_desc(&tq);
-      ptx::tma_prefetch_desc(&tdo);
-      ptx::mbar_arrive_expect_tx(&bar_kv, 2 * C::TILE);
-      tma_tile<D>(sK, &tk, &bar_kv, j * kBc, h, b);
-      tma_tile<D>(sV, &tv, &bar_kv, j * kBc, h, b);
-    }
+    ptx::tma_prefetch_desc(&tq);
+    ptx::tma_prefetch_desc(&tdo);
+    ptx::mbar_arrive_expect_tx_elect(&bar_kv, 2 * C::TILE);
+    tma_tile<D>(sK, &tk, &bar_kv, j * kBc, h, b);
+    tma_tile<D>(sV, &tv, &bar_kv, j * kBc, h, b);
     for (int k = 0; k < cnt; ++k) {
       const int ib = list[k], st = k % NST;
       uint8_t* stg = sStage + st * STAGE;
@@ -488,41 +478,37 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
         dl_s[lane * 4 + e] = rr < g.N ? delta[(long long)bh * g.N + rr] : 0.f;
       }
       __syncwarp();
-      if (lane == 0) {
-        ptx::mbar_arrive_expect_tx(&qd_full[st], 2 * C::TILE);
-        tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
-        tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
-      }
+      ptx::mbar_arrive_expect_tx_elect(&qd_full[st], 2 * C::TILE);
+      tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
+      tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
       __syncwarp();
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      ptx::mbar_wait(&bar_kv, 0);
-      auto issue_sdp = [&](int k) {
-        const int st = k % NST;
-        const uint8_t* stg = sStage + st * STAGE;
-        ptx::mbar_wait(&qd_full[st], (k / NST) & 1);
-        if (!ALIAS) ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
-        mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
-        ptx::mma_commit(&s_full);
-      };
-      if (cnt > 0) issue_sdp(0);
-      for (int k = 0; k < cnt; ++k) {
-        if (!ALIAS && k + 1 < cnt) issue_sdp(k + 1);
-        const int st = k % NST;
-        const uint8_t* stg = sStage + st * STAGE;
-        ptx::mbar_wait(&p_full, k & 1);
-        ptx::tc_fence_after();
-        mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
-        mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
-        ptx::mma_commit(&qd_empty[st]);
-        ptx::mma_commit(&p_empty);
-        if (ALIAS && k + 1 < cnt) issue_sdp(k + 1);
-      }
-      ptx::mma_commit(&acc_full);
+    ptx::mbar_wait(&bar_kv, 0);
+    auto issue_sdp = [&](int k) {
+      const int st = k % NST;
+      const uint8_t* stg = sStage + st * STAGE;
+      ptx::mbar_wait(&qd_full[st], (k / NST) & 1);
+      if (!ALIAS) ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
+      ptx::tc_fence_after();
+      mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
+      mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
+      ptx::mma_commit_elect(&s_full);
+    };
+    if (cnt > 0) issue_sdp(0);
+    for (int k = 0; k < cnt; ++k) {
+      if (!ALIAS && k + 1 < cnt) issue_sdp(k + 1);
+      const int st = k % NST;
+      const uint8_t* stg = sStage + st * STAGE;
+      ptx::mbar_wait(&p_full, k & 1);
+      ptx::tc_fence_after();
+      mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
+      mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
+      ptx::mma_commit_elect(&qd_empty[st]);
+      ptx::mma_commit_elect(&p_empty);
+      if (ALIAS && k + 1 < cnt) issue_sdp(k + 1);
     }
+    ptx::mma_commit_elect(&acc_full);
   } else {
     const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
     const int key = j * kBc + r;

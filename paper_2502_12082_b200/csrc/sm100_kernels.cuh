@@ -41,7 +41,7 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 template <int D>
 __device__ __forceinline__ void tma_tile(uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int row0, int h, int b) {
 #pragma unroll
-  for (int c = 0; c < Cfg<D>::KCH; ++c) ptx::tma_load_4d(dst + c * kChunkBytes, m, bar, c * 64, row0, h, b);
+  for (int c = 0; c < Cfg<D>::KCH; ++c) ptx::tma_load_4d_elect(dst + c * kChunkBytes, m, bar, c * 64, row0, h, b);
 }
 
 // D[tmem] (+)= A·Bᵀ, A and B both [128 × D] K-major tiles (contraction over d)
@@ -52,7 +52,7 @@ __device__ __forceinline__ void mma_rows_x_rows(uint32_t d_tmem, const uint8_t* 
 #pragma unroll
   for (int ks = 0; ks < Cfg<D>::KSTEPS; ++ks) {
     const uint32_t off = (ks >> 2) * kChunkBytes + (ks & 3) * 32;
-    ptx::mma_bf16_ss(d_tmem, ptx::sdesc_kmajor(sa + off), ptx::sdesc_kmajor(sb + off), idesc,
+    ptx::mma_bf16_ss_elect(d_tmem, ptx::sdesc_kmajor(sa + off), ptx::sdesc_kmajor(sb + off), idesc,
                      (accum_first || ks > 0) ? 1u : 0u);
   }
 }
@@ -67,7 +67,7 @@ __device__ __forceinline__ void mma_p_x_tile(uint32_t d_tmem, const uint8_t* a, 
   for (int ks = 0; ks < 8; ++ks) {
     const uint32_t aoff = (ks >> 2) * kChunkBytes + (ks & 3) * 32;
     const uint32_t boff = ks * 2048;
-    ptx::mma_bf16_ss(d_tmem, ptx::sdesc_kmajor(sa + aoff), ptx::sdesc_mnmajor(sb + boff, kChunkBytes), idesc,
+    ptx::mma_bf16_ss_elect(d_tmem, ptx::sdesc_kmajor(sa + aoff), ptx::sdesc_mnmajor(sb + boff, kChunkBytes), idesc,
                      (accumulate || ks > 0) ? 1u : 0u);
   }
 }

@@ -18,6 +18,7 @@
 #pragma once
 
 #include "sm100_kernels.cuh"
+#include "trace.cuh"
 
 namespace entmax {
 namespace sm100 {
@@ -42,8 +43,14 @@ struct TauSmem {
   static size_t bytes(int Tc) { return fixed + 4 * (size_t)Tc + 64; }   // cflag, aflag (u8) + cblk (u16)
 };
 
+// Launched as clusters of two CTAs = two adjacent query blocks of the same head, which stream the
+// same K blocks: each CTA TMA-loads half of every K tile (64 rows) with .multicast::cluster, so an SM
+// issues 8 KB per tile instead of 16 KB (TMA issue on the SM is what slows the tensor pipe down,
+// see DESIGN.md §6).  MMA completions are committed to the empty barriers of both CTAs.
+// `tk` is a tensor map with 64-row boxes.  Grid x is rounded up to even; a CTA past T_r streams and
+// computes but writes nothing.
 template <int D, int E>
-__global__ void __launch_bounds__(kTauThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTauThreads, 1)
 tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, Geom g, AlphaParams ap,
            int n_iter, float* __restrict__ tau_out, int32_t* __restrict__ cand_cnt, int32_t* __restrict__ cand_idx) {
   using C = Cfg<D>;
@@ -59,27 +66,31 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   uint8_t* cflag = reinterpret_cast<uint8_t*>(xch + 4 * kTauMath);         // [Tc] candidate blocks (τ_lo)
   uint8_t* aflag = cflag + g.Tc;                                           // [Tc] exact active blocks
   uint16_t* cblk = reinterpret_cast<uint16_t*>(aflag + g.Tc);            // [Tc] fallback block list (2·Tc even)
-  __shared__ __align__(8) uint64_t bar_q, k_full[NST], k_empty[NST], s_full[kTauSBuf], s_empty[kTauSBuf], dec_bar;
+  __shared__ __align__(8) uint64_t bar_q, k_full[NST], k_empty[NST], s_full[kTauSBuf], s_empty[kTauSBuf], dec_bar,
+      x_bar;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int s_fallback, s_ncb, s_overflow;
+  __shared__ int s_fallback, s_ncb, s_overflow, s_peer_overflow;
 
   const int i = blockIdx.x, bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = g.visible_kblocks(i);
+  const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
+  const bool real_cta = i < g.Tr;
+  const int nkb = g.visible_kblocks(min((i | 1), g.Tr - 1));   // identical for both CTAs of the pair
   const long long li = (long long)bh * g.Tr + i;
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
     for (int s = 0; s < NST; ++s) {
       ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&k_empty[s], 1);
+      ptx::mbar_init(&k_empty[s], 2);      // one MMA commit from each CTA of the pair
     }
     for (int s = 0; s < kTauSBuf; ++s) {
       ptx::mbar_init(&s_full[s], 1);
       ptx::mbar_init(&s_empty[s], 8);
     }
     ptx::mbar_init(&dec_bar, 1);
+    ptx::mbar_init(&x_bar, 1);
     ptx::fence_mbar_init();
     s_overflow = 0;
   }
@@ -89,52 +100,55 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   }
   if (warp == 9) ptx::tmem_alloc<128 * kTauSBuf>(&tmem_base_sh);
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();   // both CTAs' barriers exist before any multicast targets them
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
   if (warp == 8) {
     // ---------------------------------------------------------------- TMA producer
-    if (lane == 0) {
-      ptx::tma_prefetch_desc(&tq);
-      ptx::tma_prefetch_desc(&tk);
-      ptx::mbar_arrive_expect_tx(&bar_q, C::TILE);
-      tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
-      int k = 0;
-      auto load = [&](int j) {
-        const int st = k % NST;
-        ptx::mbar_wait(&k_empty[st], ((k / NST) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&k_full[st], C::TILE);
-        tma_tile<D>(sK + st * C::TILE, &tk, &k_full[st], j * kBc, h, b);
-        ++k;
-      };
-      for (int p = 0; p < 2; ++p)
-        for (int j = 0; j < nkb; ++j) load(j);
-      ptx::mbar_wait(&dec_bar, 0);
-      if (s_fallback)
-        for (int t = 0; t < n_iter; ++t)
-          for (int c = 0; c < s_ncb; ++c) load(cblk[c]);
-    }
+    ptx::tma_prefetch_desc(&tq);
+    ptx::tma_prefetch_desc(&tk);
+    ptx::mbar_arrive_expect_tx_elect(&bar_q, C::TILE);
+    tma_tile<D>(sQ, &tq, &bar_q, i * kBr, h, b);
+    int k = 0;
+    auto load = [&](int j) {
+      const int st = k % NST;
+      ptx::mbar_wait(&k_empty[st], ((k / NST) & 1) ^ 1);
+      ENTMAX_TRACE_EV(6144 + k);
+      ptx::mbar_arrive_expect_tx_elect(&k_full[st], C::TILE);   // both halves land here
+#pragma unroll
+      for (int c = 0; c < C::KCH; ++c)
+        ptx::tma_load_4d_mc_elect(sK + st * C::TILE + c * kChunkBytes + rank * (kChunkBytes / 2), &tk, &k_full[st], c * 64,
+                            j * kBc + (int)rank * 64, h, b, 0x3);
+      ++k;
+    };
+    for (int p = 0; p < 2; ++p)
+      for (int j = 0; j < nkb; ++j) load(j);
+    ptx::mbar_wait(&dec_bar, 0);
+    if (s_fallback)
+      for (int t = 0; t < n_iter; ++t)
+        for (int c = 0; c < s_ncb; ++c) load(cblk[c]);
   } else if (warp == 9) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      ptx::mbar_wait(&bar_q, 0);
-      int k = 0;
-      auto mma = [&]() {
-        const int st = k % NST, sb = k % kTauSBuf;
-        ptx::mbar_wait(&k_full[st], (k / NST) & 1);
-        ptx::mbar_wait(&s_empty[sb], ((k / kTauSBuf) & 1) ^ 1);
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(tmem + sb * 128, sQ, sK + st * C::TILE, false);
-        ptx::mma_commit(&k_empty[st]);
-        ptx::mma_commit(&s_full[sb]);
-        ++k;
-      };
-      for (int p = 0; p < 2 * nkb; ++p) mma();
-      ptx::mbar_wait(&dec_bar, 0);
-      if (s_fallback)
-        for (int p = 0; p < n_iter * s_ncb; ++p) mma();
-    }
+    ptx::mbar_wait(&bar_q, 0);
+    int k = 0;
+    auto mma = [&]() {
+      const int st = k % NST, sb = k % kTauSBuf;
+      ENTMAX_TRACE_EV(4 * k);
+      ptx::mbar_wait(&k_full[st], (k / NST) & 1);
+      ENTMAX_TRACE_EV(4 * k + 1);
+      ptx::mbar_wait(&s_empty[sb], ((k / kTauSBuf) & 1) ^ 1);
+      ENTMAX_TRACE_EV(4 * k + 2);
+      ptx::tc_fence_after();
+      mma_rows_x_rows<D>(tmem + sb * 128, sQ, sK + st * C::TILE, false);
+      ptx::mma_commit_mc_elect(&k_empty[st], 0x3);
+      ptx::mma_commit_elect(&s_full[sb]);
+      ++k;
+    };
+    for (int p = 0; p < 2 * nkb; ++p) mma();
+    ptx::mbar_wait(&dec_bar, 0);
+    if (s_fallback)
+      for (int p = 0; p < n_iter * s_ncb; ++p) mma();
   } else {
     // ---------------------------------------------------------------- math warps (256 threads)
     const int tid = threadIdx.x;
@@ -149,14 +163,22 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     // read this thread's 64 scores of step k (columns hf*64 .. +63 of key block j), masked
     auto read_tile = [&](int j, float (&s)[64]) {
       const int sb = k % kTauSBuf;
+      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k);
       ptx::mbar_wait(&s_full[sb], (k / kTauSBuf) & 1);
+      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k + 1);
       ptx::tc_fence_after();
       uint32_t ra[32], rb[32];
+#ifdef ENTMAX_TRACE_NOLD
+#pragma unroll
+      for (int e = 0; e < 32; ++e) ra[e] = rb[e] = 0u;
+#else
       ptx::tmem_ld32(lane_base + sb * 128, ra);
       ptx::tmem_ld32(lane_base + sb * 128 + 32, rb);
       ptx::tmem_wait_ld();
+#endif
       ptx::tc_fence_before();
       warp_arrive(&s_empty[sb]);
+      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k + 2);
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
         s[e] = __uint_as_float(ra[e]);
@@ -218,7 +240,15 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
     if (cnt > kTauCap) s_overflow = 1;
     ptx::named_bar_sync(1, kTauMath);
-    const bool fallback = s_overflow != 0;
+    // the pair shares the K stream, so the fallback decision is exchanged and made jointly
+    if (tid == 0) {
+      ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&s_peer_overflow), peer), (uint32_t)s_overflow);
+      ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&x_bar), peer));
+      ptx::mbar_wait_cluster(&x_bar, 0);
+      s_fallback = (s_overflow | s_peer_overflow) ? 1 : 0;
+    }
+    ptx::named_bar_sync(1, kTauMath);
+    const bool fallback = s_fallback != 0;
 
     if (!fallback) {
       // ---- T iterations of Alg. 1 on the compact lists (one thread per row: hf == 0)
@@ -244,35 +274,26 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         }
       }
       ptx::named_bar_sync(1, kTauMath);
-      if (warp == 0) {
+      if (warp == 0 && real_cta) {
         const int n = compact_flags(aflag, nkb, cand_idx + li * g.Tc);
         if (lane == 0) cand_cnt[li] = n;
       }
       if (tid == 0) {
-        s_fallback = 0;
         __threadfence_block();
         ptx::mbar_arrive(&dec_bar);
       }
     } else {
-      // ---- fallback: streaming Alg. 3 passes over the candidate blocks
+      // ---- fallback: streaming Alg. 3 passes over every visible block (the pair streams the same
+      // blocks, so no per-CTA pruning); the output kernel gets this CTA's τ_lo candidate blocks
       if (warp == 0) {
-        int n = 0;
-        for (int base = 0; base < nkb; base += 32) {
-          const int j = base + lane;
-          const bool f = j < nkb && cflag[j];
-          const uint32_t m = __ballot_sync(0xffffffffu, f);
-          if (f) cblk[n + __popc(m & ((1u << lane) - 1u))] = (uint16_t)j;
-          n += __popc(m);
-        }
-        if (lane == 0) {
-          s_ncb = n;
-          s_fallback = 1;
-          cand_cnt[li] = n;
+        for (int c = lane; c < nkb; c += 32) cblk[c] = (uint16_t)c;
+        if (real_cta) {
+          const int n = compact_flags(cflag, nkb, cand_idx + li * g.Tc);
+          if (lane == 0) cand_cnt[li] = n;
         }
         __syncwarp();
-        for (int c = lane; c < n; c += 32) cand_idx[li * g.Tc + c] = cblk[c];
-        __syncwarp();
         if (lane == 0) {
+          s_ncb = nkb;
           __threadfence_block();
           ptx::mbar_arrive(&dec_bar);
         }
@@ -310,7 +331,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  ptx::cluster_sync();   // no CTA leaves while its peer may still multicast into it
   if (warp == 9) ptx::tmem_dealloc<128 * kTauSBuf>(tmem);
 }
 
