@@ -280,7 +280,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
 
   const int i = blockIdx.x, bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const long long li = (long long)bh * g.Tr + i;
   const int cnt = row_cnt[li];
   const int32_t* list = row_idx + li * g.Tc;
