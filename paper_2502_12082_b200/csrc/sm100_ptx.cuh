@@ -56,6 +56,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// the same on a precomputed 32-bit shared address (keeps address conversion out of hot loops)
+__device__ __forceinline__ void mbar_wait_addr(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void mbar_arrive_addr(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
@@ -333,6 +349,49 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 __device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+// scalar shared-memory accesses by 32-bit shared address (keeps the compiler on STS/LDS when the
+// pointer arithmetic would otherwise lose the address space); *_pred store only where p != 0
+__device__ __forceinline__ void st_shared_f32_pred(uint32_t saddr, float v, uint32_t p) {
+  asm volatile("{.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}" ::"r"(saddr), "f"(v),
+               "r"(p) : "memory");
+}
+__device__ __forceinline__ void st_shared_u16_pred(uint32_t saddr, uint32_t v, uint32_t p) {
+  asm volatile("{.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n\t}" ::"r"(saddr),
+               "h"((unsigned short)v), "r"(p) : "memory");
+}
+__device__ __forceinline__ void st_shared_f2_pred(uint32_t saddr, float2 v, uint32_t p) {
+  asm volatile("{.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.shared.v2.f32 [%0], {%1, %2};\n\t}" ::"r"(saddr),
+               "f"(v.x), "f"(v.y), "r"(p) : "memory");
+}
+// list append: if v > thr, store v at [as] and the u16 tag at [aj], then advance as by 1024 and aj
+// by 512 (one predicate, no branch; the layout of the τ kernel's per-thread candidate lists)
+__device__ __forceinline__ void append_if_gt(uint32_t& as, uint32_t& aj, float v, float thr, uint32_t tag) {
+  asm volatile(
+      "{.reg .pred q;\n\tsetp.gt.f32 q, %2, %3;\n\t@q st.shared.f32 [%0], %2;\n\t@q st.shared.u16 [%1], %4;\n\t"
+      "@q add.u32 %0, %0, 1024;\n\t@q add.u32 %1, %1, 512;\n\t}"
+      : "+r"(as), "+r"(aj)
+      : "f"(v), "f"(thr), "h"((unsigned short)tag)
+      : "memory");
+}
+__device__ __forceinline__ float2 ld_shared_f2(uint32_t saddr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t saddr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t saddr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_shared_u16(uint32_t saddr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(saddr) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {

@@ -3,18 +3,21 @@
 // Paper: Alg. 1 per row, Alg. 3 per query block: one pass for the row
 // max, then T passes accumulating f, f', f'' (Eqs. 3, 6, 7) over all K blocks (Eq. 8).
 //
-// B200 design (same result, fewer passes): after pass 0 (row max m, bracket τ_lo = m − 1), pass 1
-// streams the K blocks once more and copies every score with (α−1)c·s > τ_lo into a per-row list
-// in shared memory.  Every other element has x = z − τ <= z − τ_lo <= 0 for every iterate τ >= τ_lo
-// (the bracket only moves up), so it contributes exact zeros to f, f', f'' (reading c7) — the T
-// Halley-bisection iterations then run on the compact lists without recomputing S.  The same
-// lists, tested against the final τ with the kernels' own fma(s, c', −τ) > 0, give the exact
-// block mask, so the output kernel only visits active blocks.  If a row's list overflows (wide
-// supports, small α), the CTA falls back to streaming passes 2..T+1 over the candidate blocks
-// (blocks holding any element above τ_lo), i.e. Alg. 3 restricted to those blocks.
-//
-// Warp roles (320 threads): warps 0-7 math (thread t: row t & 127, column half t >> 7 of each
-// 128-key tile; warp w reads TMEM lanes 32·(w & 3)), warp 8 TMA producer, warp 9 MMA issuer.
+// B200 design (same result, one pass over K in the common case): the K blocks stream once; the
+// threads of a row keep a running max m_run of the row and append every score with
+// c'·s > τ_lo(m_run) = c'·m_run − 1 to the row's candidate list in shared memory.  m_run <= m, so
+// τ_lo(m_run) <= τ_lo(m) and every score the final filter needs is kept; everything else has
+// x = z − τ <= z − τ_lo(m) <= 0 for every iterate τ >= τ_lo(m) (the bracket only moves up) and
+// contributes exact zeros to f, f', f'' (reading c7).  The T Halley-bisection iterations then run
+// on the lists without recomputing S.  The same lists, tested against the final τ with the kernels'
+// own fma(s, c', −τ) > 0, give the exact block mask, so the output kernel only visits active blocks.
+// The first W blocks only raise the running max and are streamed again at the end (fewer transient
+// candidates).  Overflow (a row list is finite): tier 1 streams K once more with the exact threshold
+// τ_lo(m); tier 2, if even that overflows (wide supports, small α), streams T more passes over all
+// visible blocks — Alg. 3 itself.
+// Warp roles (576 threads): warps 0-15 math (thread t: row t & 127, column quarter t >> 7 of each
+// 128-key tile; warp w reads TMEM lanes 32·(w & 3)) — four warps per SM sub-partition hide the
+// latency of the short compare/branch chains; warp 16 TMA producer, warp 17 MMA issuer.
 #pragma once
 
 #include "sm100_kernels.cuh"
@@ -23,9 +26,9 @@
 namespace entmax {
 namespace sm100 {
 
-constexpr int kTauThreads = 320;
-constexpr int kTauMath = 256;
-constexpr int kTauCap = 80;  // list slots per (row, column half); the count has a heavy tail
+constexpr int kTauMathWarps = 16;
+constexpr int kTauMath = 32 * kTauMathWarps;
+constexpr int kTauThreads = kTauMath + 64;
 constexpr int kTauSBuf = 4;  // S tiles in flight in TMEM (4 × 128 columns)
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
@@ -34,13 +37,35 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
+// Row-list append: if v > thr, take slot = cnt++ (shared atomic; the row's four threads append
+// concurrently) and store (v, tag) there when slot < cap.  Lists are slot-major: [slot][128 rows];
+// tag = key block << 2 | column quarter of the appending thread.
+__device__ __forceinline__ void row_append(uint32_t cnt_addr, uint32_t ls_row, uint32_t lj_row, float v, float thr,
+                                           uint32_t tag, uint32_t cap) {
+  asm volatile(
+      "{\n\t.reg .pred q, w;\n\t.reg .u32 slot, a;\n\t"
+      "mov.u32 slot, 0;\n\t"
+      "setp.gt.f32 q, %3, %4;\n\t"
+      "@q atom.shared.add.u32 slot, [%0], 1;\n\t"
+      "setp.lt.and.u32 w, slot, %6, q;\n\t"
+      "mad.lo.u32 a, slot, 512, %1;\n\t"
+      "@w st.shared.f32 [a], %3;\n\t"
+      "mad.lo.u32 a, slot, 256, %2;\n\t"
+      "@w st.shared.u16 [a], %5;\n\t}" ::"r"(cnt_addr),
+      "r"(ls_row), "r"(lj_row), "f"(v), "f"(thr), "h"((unsigned short)tag), "r"(cap)
+      : "memory");
+}
+
 template <int D>
 struct TauSmem {
-  static constexpr int NST = (D == 64) ? 4 : 2;   // K-tile ring depth
+  static constexpr int NST = (D == 64) ? 3 : 2;   // K-tile ring depth
+  // list slots per row: the online pass appends ~37 scores per row on average for the paper's
+  // Gaussian rows at N = 8192 (max ~140); the exact-threshold count has a heavy tail (DESIGN.md §τ)
+  static constexpr int CAP = (D == 64) ? 190 : 146;
   static constexpr size_t tiles = (size_t)(1 + NST) * Cfg<D>::TILE;
-  static constexpr size_t lists = (size_t)(kTauCap + 1) * kTauMath * (4 + 2);   // + scratch slot
-  static constexpr size_t fixed = 1024 + tiles + lists + kTauMath * 4 * 4;  // + exchange scratch
-  static size_t bytes(int Tc) { return fixed + 4 * (size_t)Tc + 64; }   // cflag, aflag (u8) + cblk (u16)
+  static constexpr size_t lists = (size_t)CAP * kBr * (4 + 2);     // score f32, key block u16
+  static constexpr size_t fixed = 1024 + tiles + lists + 3 * kTauMath * 8 + 2 * kBr * 4;
+  static size_t bytes(int Tc) { return fixed + 2 * (size_t)Tc + 64; }   // cflag, aflag (u8)
 };
 
 // Launched as clusters of two CTAs = two adjacent query blocks of the same head, which stream the
@@ -56,20 +81,23 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   using C = Cfg<D>;
   using SM = TauSmem<D>;
   constexpr int NST = SM::NST;
+  constexpr int kCap = SM::CAP;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sK = sQ + C::TILE;
-  float* list_s = reinterpret_cast<float*>(sK + NST * C::TILE);           // [CAP+1][256]
-  uint16_t* list_j = reinterpret_cast<uint16_t*>(list_s + (kTauCap + 1) * kTauMath);  // [CAP+1][256]
-  float* xch = reinterpret_cast<float*>(list_j + (kTauCap + 1) * kTauMath);      // [4][256] exchange
-  uint8_t* cflag = reinterpret_cast<uint8_t*>(xch + 4 * kTauMath);         // [Tc] candidate blocks (τ_lo)
-  uint8_t* aflag = cflag + g.Tc;                                           // [Tc] exact active blocks
-  uint16_t* cblk = reinterpret_cast<uint16_t*>(aflag + g.Tc);            // [Tc] fallback block list (2·Tc even)
+  float* list_s = reinterpret_cast<float*>(sK + NST * C::TILE);            // [CAP][128] scores
+  uint16_t* list_j = reinterpret_cast<uint16_t*>(list_s + kCap * kBr);      // [CAP][128] key block
+  float* xch = reinterpret_cast<float*>(list_j + kCap * kBr);               // [3][512] exchange (8-byte slots)
+  uint64_t* xch64 = reinterpret_cast<uint64_t*>(xch);
+  float* mshare = xch + 6 * kTauMath;                                        // [128] running row maxima
+  int* rowcnt = reinterpret_cast<int*>(mshare + kBr);                        // [128] list lengths
+  uint8_t* cflag = reinterpret_cast<uint8_t*>(rowcnt + kBr);                 // [Tc] candidate blocks (τ_lo)
+  uint8_t* aflag = cflag + g.Tc;                                             // [Tc] exact active blocks
   __shared__ __align__(8) uint64_t bar_q, k_full[NST], k_empty[NST], s_full[kTauSBuf], s_empty[kTauSBuf], dec_bar,
       x_bar;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int s_fallback, s_ncb, s_overflow, s_peer_overflow;
+  __shared__ int s_fallback, s_overflow, s_peer_overflow[2];
 
   const int i = blockIdx.x, bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
@@ -78,6 +106,8 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const bool real_cta = i < g.Tr;
   const int nkb = g.visible_kblocks(min((i | 1), g.Tr - 1));   // identical for both CTAs of the pair
   const long long li = (long long)bh * g.Tr + i;
+  // warm-up: the first W blocks only raise the running max and are streamed again at the end
+  const int W = nkb >= 32 ? max(4, nkb / 8) : nkb / 8;
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
@@ -87,7 +117,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
     for (int s = 0; s < kTauSBuf; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_empty[s], 8);
+      ptx::mbar_init(&s_empty[s], kTauMathWarps);
     }
     ptx::mbar_init(&dec_bar, 1);
     ptx::mbar_init(&x_bar, 1);
@@ -98,13 +128,17 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     cflag[j] = 0;
     aflag[j] = 0;
   }
-  if (warp == 9) ptx::tmem_alloc<128 * kTauSBuf>(&tmem_base_sh);
+  if (threadIdx.x < kBr) {
+    mshare[threadIdx.x] = -INFINITY;
+    rowcnt[threadIdx.x] = 0;
+  }
+  if (warp == kTauMathWarps + 1) ptx::tmem_alloc<128 * kTauSBuf>(&tmem_base_sh);
   ptx::tc_fence_before();
   ptx::cluster_sync();   // both CTAs' barriers exist before any multicast targets them
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
 
-  if (warp == 8) {
+  if (warp == kTauMathWarps) {
     // ---------------------------------------------------------------- TMA producer
     ptx::tma_prefetch_desc(&tq);
     ptx::tma_prefetch_desc(&tk);
@@ -118,17 +152,20 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::mbar_arrive_expect_tx_elect(&k_full[st], C::TILE);   // both halves land here
 #pragma unroll
       for (int c = 0; c < C::KCH; ++c)
-        ptx::tma_load_4d_mc_elect(sK + st * C::TILE + c * kChunkBytes + rank * (kChunkBytes / 2), &tk, &k_full[st], c * 64,
-                            j * kBc + (int)rank * 64, h, b, 0x3);
+        ptx::tma_load_4d_mc_elect(sK + st * C::TILE + c * kChunkBytes + rank * (kChunkBytes / 2), &tk, &k_full[st],
+                                  c * 64, j * kBc + (int)rank * 64, h, b, 0x3);
       ++k;
     };
-    for (int p = 0; p < 2; ++p)
-      for (int j = 0; j < nkb; ++j) load(j);
+    for (int t = 0; t < nkb + W; ++t) load(t < nkb ? t : t - nkb);
     ptx::mbar_wait(&dec_bar, 0);
-    if (s_fallback)
-      for (int t = 0; t < n_iter; ++t)
-        for (int c = 0; c < s_ncb; ++c) load(cblk[c]);
-  } else if (warp == 9) {
+    if (s_fallback) {
+      for (int j = 0; j < nkb; ++j) load(j);                 // tier 1
+      ptx::mbar_wait(&dec_bar, 1);
+      if (s_fallback > 1)
+        for (int t = 0; t < n_iter; ++t)
+          for (int j = 0; j < nkb; ++j) load(j);             // tier 2
+    }
+  } else if (warp == kTauMathWarps + 1) {
     // ---------------------------------------------------------------- MMA issuer
     ptx::mbar_wait(&bar_q, 0);
     int k = 0;
@@ -145,194 +182,281 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::mma_commit_elect(&s_full[sb]);
       ++k;
     };
-    for (int p = 0; p < 2 * nkb; ++p) mma();
+    for (int p = 0; p < nkb + W; ++p) mma();
     ptx::mbar_wait(&dec_bar, 0);
-    if (s_fallback)
-      for (int p = 0; p < n_iter * s_ncb; ++p) mma();
+    if (s_fallback) {
+      for (int p = 0; p < nkb; ++p) mma();
+      ptx::mbar_wait(&dec_bar, 1);
+      if (s_fallback > 1)
+        for (int p = 0; p < n_iter * nkb; ++p) mma();
+    }
   } else {
-    // ---------------------------------------------------------------- math warps (256 threads)
+    // ---------------------------------------------------------------- math warps (512 threads)
     const int tid = threadIdx.x;
-    const int r = tid & 127, hf = tid >> 7;
+    const int r = tid & 127, qc = tid >> 7;
     const int row = i * kBr + r;
     const bool valid = row < g.N;
     const int my_last = g.causal ? row : g.N - 1;
     const int cta_last = g.causal ? i * kBr : g.N - 1;
-    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + hf * 64;
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + qc * 32;
     int k = 0;
+    const uint32_t sfull0 = ptx::smem_u32(&s_full[0]), sempty0 = ptx::smem_u32(&s_empty[0]);
 
-    // read this thread's 64 scores of step k (columns hf*64 .. +63 of key block j), masked
-    auto read_tile = [&](int j, float (&s)[64]) {
+    // read this thread's 32 scores of step k (columns qc*32 .. +31 of key block j), masked
+    auto read_tile = [&](int j, float (&s)[32]) {
       const int sb = k % kTauSBuf;
       if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k);
-      ptx::mbar_wait(&s_full[sb], (k / kTauSBuf) & 1);
+      ptx::mbar_wait_addr(sfull0 + 8 * sb, (k / kTauSBuf) & 1);
       if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k + 1);
       ptx::tc_fence_after();
-      uint32_t ra[32], rb[32];
+      uint32_t ra[32];
 #ifdef ENTMAX_TRACE_NOLD
 #pragma unroll
-      for (int e = 0; e < 32; ++e) ra[e] = rb[e] = 0u;
+      for (int e = 0; e < 32; ++e) ra[e] = 0u;
 #else
       ptx::tmem_ld32(lane_base + sb * 128, ra);
-      ptx::tmem_ld32(lane_base + sb * 128 + 32, rb);
       ptx::tmem_wait_ld();
 #endif
       ptx::tc_fence_before();
-      warp_arrive(&s_empty[sb]);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_addr(sempty0 + 8 * sb);
       if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k + 2);
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        s[e] = __uint_as_float(ra[e]);
-        s[32 + e] = __uint_as_float(rb[e]);
-      }
+      for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(ra[e]);
       if ((j + 1) * kBc - 1 > cta_last) {
-        const int key0 = j * kBc + hf * 64;
+        const int key0 = j * kBc + qc * 32;
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
+        for (int e = 0; e < 32; ++e)
           if (key0 + e > my_last) s[e] = -INFINITY;
       }
       ++k;
     };
 
-    // ---- pass 0: row max (Alg. 1 line 4)
-    float smax = -INFINITY;
-    for (int j = 0; j < nkb; ++j) {
-      float s[64];
-      read_tile(j, s);
-#pragma unroll
-      for (int e = 0; e < 64; e += 2) smax = fmax3(smax, s[e], s[e + 1]);
-    }
-    xch[tid] = smax;
-    ptx::named_bar_sync(1, kTauMath);
-    smax = fmaxf(xch[r], xch[128 + r]);
-    const float n_vis = g.causal ? (float)(row + 1) : (float)g.N;
-    RowState rs = bracket_init(smax * ap.cp, n_vis, ap.alpha);
-    // conservative score threshold: s <= thr ⇒ fma(s, c', −τ_lo) <= 0 (margin >> fma rounding)
-    const float thr = (rs.lo - fmaxf(fabsf(rs.lo), 1e-6f) * 3.0e-6f) / ap.cp;
+    // the two CTAs of the pair stream the same K blocks, so every fallback decision is joint
+    // (s_overflow is read after the barrier: every thread's write to it must be visible)
+    auto pair_any = [&](int use) {
+      ptx::named_bar_sync(1, kTauMath);
+      if (tid == 0) {
+        const int flag = s_overflow;
+        ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&s_peer_overflow[use]), peer), (uint32_t)flag);
+        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&x_bar), peer));
+        ptx::mbar_wait_cluster(&x_bar, use);
+        s_fallback = (flag | s_peer_overflow[use]) ? 1 + use : 0;
+      }
+      ptx::named_bar_sync(1, kTauMath);
+      return s_fallback != 0;
+    };
 
-    // ---- pass 1: compact the candidates z > τ_lo into this thread's list
-    int cnt = 0;
-    for (int j = 0; j < nkb; ++j) {
-      float s[64];
-      read_tile(j, s);
-      // groups of 8 keys: a group max (FMNMX3) decides whether the short, branch-free append
-      // runs; candidates are rare (~1e-3 of the keys for Gaussian rows at α = 1.5)
-      const float thr_v = valid ? thr : INFINITY;
-      bool any = false;
+    // Σ over the row's four column quarters in a fixed order (every thread of the row gets the
+    // identical sums, so the four Alg. 1 updates agree bit for bit)
+    auto row_sum3 = [&](float& a0, float& a1, float& a2) {
+      ptx::named_bar_sync(1, kTauMath);
+      xch[tid] = a0;
+      xch[kTauMath + tid] = a1;
+      xch[2 * kTauMath + tid] = a2;
+      ptx::named_bar_sync(1, kTauMath);
+      a0 = (xch[r] + xch[128 + r]) + (xch[256 + r] + xch[384 + r]);
+      a1 = (xch[kTauMath + r] + xch[kTauMath + 128 + r]) + (xch[kTauMath + 256 + r] + xch[kTauMath + 384 + r]);
+      a2 = (xch[2 * kTauMath + r] + xch[2 * kTauMath + 128 + r]) +
+           (xch[2 * kTauMath + 256 + r] + xch[2 * kTauMath + 384 + r]);
+    };
+
+    // the same for 64-bit fixed-point partial sums (integer adds: the combined sum is exact)
+    auto row_sum3_fx = [&](uint64_t& a0, uint64_t& a1, uint64_t& a2) {
+      ptx::named_bar_sync(1, kTauMath);
+      xch64[tid] = a0;
+      xch64[kTauMath + tid] = a1;
+      xch64[2 * kTauMath + tid] = a2;
+      ptx::named_bar_sync(1, kTauMath);
+      a0 = xch64[r] + xch64[128 + r] + xch64[256 + r] + xch64[384 + r];
+      a1 = xch64[kTauMath + r] + xch64[kTauMath + 128 + r] + xch64[kTauMath + 256 + r] + xch64[kTauMath + 384 + r];
+      a2 = xch64[2 * kTauMath + r] + xch64[2 * kTauMath + 128 + r] + xch64[2 * kTauMath + 256 + r] +
+           xch64[2 * kTauMath + 384 + r];
+    };
+
+    const uint32_t ls_row = ptx::smem_u32(list_s) + r * 4;     // slot c at + c·512
+    const uint32_t lj_row = ptx::smem_u32(list_j) + r * 2;     // slot c at + c·256
+    const uint32_t cnt_addr = ptx::smem_u32(rowcnt) + r * 4;
+    const uint32_t msh = ptx::smem_u32(mshare) + r * 4;
+    const float inv_cp = 1.0f / ap.cp;    // (the 3e-6 margin dwarfs the product's rounding)
+    // conservative score threshold: s <= thr(m) ⇒ fma(s, c', −τ_lo(m)) <= 0 (margin >> fma rounding)
+    auto thr_of = [&](float m) {
+      const float lo = m * ap.cp - 1.0f;
+      return valid ? (lo - fmaxf(fabsf(lo), 1e-6f) * 3.0e-6f) * inv_cp : INFINITY;
+    };
+
+    // One streaming pass appending the scores above the threshold to the row lists.
+    // online: the threshold follows the running max of the row (own quarter + the row's published
+    // value: a benign race, any value read is a lower bound of m); the first W blocks only raise
+    // the max and are appended when they stream again at the end.  !online: fixed threshold `thr`.
+    float mrun = -INFINITY, thr = thr_of(-INFINITY);
+    auto stream_pass = [&](bool online) {
+      const int nsteps = online ? nkb + W : nkb;
+      for (int t = 0; t < nsteps; ++t) {
+        const int j = t < nkb ? t : t - nkb;
+        float s[32];
+        read_tile(j, s);
+        float gm[4];
 #pragma unroll
-      for (int gq = 0; gq < 8; ++gq) {
-        const float* sg = s + 8 * gq;
-        const float gm = fmax3(fmax3(sg[0], sg[1], sg[2]), fmax3(sg[3], sg[4], sg[5]), fmaxf(sg[6], sg[7]));
-        if (gm > thr_v) {
-          any = true;
+        for (int gq = 0; gq < 4; ++gq) {
+          const float* sg = s + 8 * gq;
+          gm[gq] = fmax3(fmax3(sg[0], sg[1], sg[2]), fmax3(sg[3], sg[4], sg[5]), fmaxf(sg[6], sg[7]));
+        }
+        if (online && t < nkb) {
+          const float tmax = fmax3(fmaxf(gm[0], gm[1]), gm[2], gm[3]);
+          const float mread = ptx::ld_shared_f32(msh);
+          const float mnew = fmax3(mrun, tmax, mread);
+          if (mnew > mrun) {
+            mrun = mnew;
+            thr = thr_of(mrun);
+          }
+          if (tmax > mread) ptx::st_shared_f32(msh, mrun);
+          if (t < W) continue;
+        }
+        uint32_t bits = 0;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const bool p = sg[e] > thr_v;
-            const int slot = min(cnt, kTauCap);            // slot kTauCap is a scratch slot
-            if (p) {
-              list_s[slot * kTauMath + tid] = sg[e];
-              list_j[slot * kTauMath + tid] = (uint16_t)j;
-            }
-            cnt += p ? 1 : 0;
+        for (int gq = 0; gq < 4; ++gq) bits |= (gm[gq] > thr) ? (1u << gq) : 0u;
+        const uint32_t wbits = __reduce_or_sync(0xffffffffu, bits);
+        if (wbits == 0) continue;
+        if (lane == 0) cflag[j] = 1;    // τ_lo candidate block (a superset when online)
+        const uint32_t tag = ((uint32_t)j << 2) | (uint32_t)qc;
+        // groups of 8 keys with a candidate in some lane: warp-uniform branch.  A lane with one hit
+        // in the group appends the group max; the per-key path runs only when some lane's
+        // second-largest key of the group is a hit too.
+#pragma unroll
+        for (int gq = 0; gq < 4; ++gq) {
+          if (!(wbits & (1u << gq))) continue;
+          const float* sg = s + 8 * gq;
+          float hh[4], ll[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            hh[q] = fmaxf(sg[2 * q], sg[2 * q + 1]);
+            ll[q] = fminf(sg[2 * q], sg[2 * q + 1]);
+          }
+          const float l01 = fmax3(fminf(hh[0], hh[1]), ll[0], ll[1]), l23 = fmax3(fminf(hh[2], hh[3]), ll[2], ll[3]);
+          const float m2 = fmax3(fminf(fmaxf(hh[0], hh[1]), fmaxf(hh[2], hh[3])), l01, l23);
+          if (__any_sync(0xffffffffu, m2 > thr)) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) row_append(cnt_addr, ls_row, lj_row, sg[e], thr, tag, kCap);
+          } else {
+            row_append(cnt_addr, ls_row, lj_row, gm[gq], thr, tag, kCap);
           }
         }
       }
-      if (__any_sync(0xffffffffu, any) && lane == 0) cflag[j] = 1;
-    }
-    if (cnt > kTauCap) s_overflow = 1;
+    };
+
+    stream_pass(true);
+    // row max m (Alg. 1 line 4) and bracket
+    xch[tid] = mrun;
     ptx::named_bar_sync(1, kTauMath);
-    // the pair shares the K stream, so the fallback decision is exchanged and made jointly
-    if (tid == 0) {
-      ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&s_peer_overflow), peer), (uint32_t)s_overflow);
-      ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&x_bar), peer));
-      ptx::mbar_wait_cluster(&x_bar, 0);
-      s_fallback = (s_overflow | s_peer_overflow) ? 1 : 0;
+    const float smax = fmax3(fmaxf(xch[r], xch[128 + r]), xch[256 + r], xch[384 + r]);
+    const float n_vis = g.causal ? (float)(row + 1) : (float)g.N;
+    RowState rs = bracket_init(smax * ap.cp, n_vis, ap.alpha);
+    thr = thr_of(smax);
+    if (qc == 0 && rowcnt[r] > kCap) s_overflow = 1;
+    bool fallback = pair_any(0);
+    if (tid == 0 && fallback) ENTMAX_TRACE_COUNT(8100);
+    if (tid == 0) ENTMAX_TRACE_COUNT(8102);
+    if (fallback) {
+      // tier 1: rebuild the lists with the exact threshold
+      if (tid == 0) {
+        ptx::mbar_arrive(&dec_bar);
+        s_overflow = 0;
+      }
+      if (qc == 0) rowcnt[r] = 0;
+      ptx::named_bar_sync(1, kTauMath);
+      stream_pass(false);
+      ptx::named_bar_sync(1, kTauMath);
+      if (qc == 0 && rowcnt[r] > kCap) s_overflow = 1;
+      fallback = pair_any(1);
+      if (tid == 0 && fallback) ENTMAX_TRACE_COUNT(8101);
     }
-    ptx::named_bar_sync(1, kTauMath);
-    const bool fallback = s_fallback != 0;
 
     if (!fallback) {
-      // ---- T iterations of Alg. 1 on the compact lists (one thread per row: hf == 0)
-      xch[tid] = __int_as_float(cnt);
-      ptx::named_bar_sync(1, kTauMath);
-      if (hf == 0) {
-        const int c0 = cnt, c1 = __float_as_int(xch[128 + r]);
-        for (int t = 0; t < n_iter; ++t) {
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-          for (int c = 0; c < c0; ++c) accum_f<E>(fmaf(list_s[c * kTauMath + r], ap.cp, -rs.tau), ap, a0, a1, a2);
-          for (int c = 0; c < c1; ++c)
-            accum_f<E>(fmaf(list_s[c * kTauMath + 128 + r], ap.cp, -rs.tau), ap, a0, a1, a2);
-          alg1_update(rs, a0, a1, a2, ap);
+      // ---- T iterations of Alg. 1 on the row lists.  The list order depends on how the row's four
+      // threads' atomics interleaved, so the sums are formed order-independently:
+      //  E ∈ {1, 2, 4}: every term [x]_+^p (p = e, e−1, e−2 >= 0) lies in [0, 1] (x <= m·c' − τ_lo = 1),
+      //    so each thread sums a strided quarter of the list in 64-bit fixed point (2^-32 units; the
+      //    rounding is far below fp32 summation error) and the integer partial sums add exactly;
+      //  generic α: each thread sums the entries it appended (tag & 3) in its own append order —
+      //    its successive slot grabs are increasing — and the quarters combine in a fixed order.
+      // Either way the result is bitwise reproducible.
+      const int n = rowcnt[r];
+      for (int t = 0; t < n_iter; ++t) {
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        if constexpr (E != 0) {
+          uint64_t q0 = 0, q1 = 0, q2 = 0;
+          for (int c = qc; c < n; c += 4) {
+            float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+            accum_f<E>(fmaf(ptx::ld_shared_f32(ls_row + c * 512), ap.cp, -rs.tau), ap, t0, t1, t2);
+            q0 += __float2ull_rn(t0 * 4294967296.0f);
+            q1 += __float2ull_rn(t1 * 4294967296.0f);
+            q2 += __float2ull_rn(t2 * 4294967296.0f);
+          }
+          row_sum3_fx(q0, q1, q2);
+          a0 = (float)q0 * 2.3283064365386963e-10f;
+          a1 = (float)q1 * 2.3283064365386963e-10f;
+          a2 = (float)q2 * 2.3283064365386963e-10f;
+        } else {
+          for (int c = 0; c < n; ++c) {
+            const bool mine = (ptx::ld_shared_u16(lj_row + c * 256) & 3u) == (uint32_t)qc;
+            const float x = fmaf(ptx::ld_shared_f32(ls_row + c * 512), ap.cp, -rs.tau);
+            accum_f<E>(mine ? x : -INFINITY, ap, a0, a1, a2);
+          }
+          row_sum3(a0, a1, a2);
         }
-        if (valid) {
-          tau_out[(long long)bh * g.N + row] = rs.tau;
-          // exact block activity from the final τ (same fma test as the output kernel)
-          for (int c = 0; c < c0; ++c)
-            if (fmaf(list_s[c * kTauMath + r], ap.cp, -rs.tau) > 0.f) aflag[list_j[c * kTauMath + r]] = 1;
-          for (int c = 0; c < c1; ++c)
-            if (fmaf(list_s[c * kTauMath + 128 + r], ap.cp, -rs.tau) > 0.f)
-              aflag[list_j[c * kTauMath + 128 + r]] = 1;
-        }
+        alg1_update(rs, a0, a1, a2, ap);
+      }
+      if (valid) {
+        if (qc == 0) tau_out[(long long)bh * g.N + row] = rs.tau;
+        // exact block activity from the final τ (same fma test as the output kernel)
+        for (int c = qc; c < n; c += 4)
+          if (fmaf(ptx::ld_shared_f32(ls_row + c * 512), ap.cp, -rs.tau) > 0.f) aflag[ptx::ld_shared_u16(lj_row + c * 256) >> 2] = 1;
       }
       ptx::named_bar_sync(1, kTauMath);
       if (warp == 0 && real_cta) {
-        const int n = compact_flags(aflag, nkb, cand_idx + li * g.Tc);
-        if (lane == 0) cand_cnt[li] = n;
+        const int nb = compact_flags(aflag, nkb, cand_idx + li * g.Tc);
+        if (lane == 0) cand_cnt[li] = nb;
       }
       if (tid == 0) {
         __threadfence_block();
         ptx::mbar_arrive(&dec_bar);
       }
     } else {
-      // ---- fallback: streaming Alg. 3 passes over every visible block (the pair streams the same
+      // ---- tier 2: streaming Alg. 3 passes over every visible block (the pair streams the same
       // blocks, so no per-CTA pruning); the output kernel gets this CTA's τ_lo candidate blocks
       if (warp == 0) {
-        for (int c = lane; c < nkb; c += 32) cblk[c] = (uint16_t)c;
         if (real_cta) {
-          const int n = compact_flags(cflag, nkb, cand_idx + li * g.Tc);
-          if (lane == 0) cand_cnt[li] = n;
+          const int nb = compact_flags(cflag, nkb, cand_idx + li * g.Tc);
+          if (lane == 0) cand_cnt[li] = nb;
         }
-        __syncwarp();
         if (lane == 0) {
-          s_ncb = nkb;
           __threadfence_block();
           ptx::mbar_arrive(&dec_bar);
         }
       }
-      ptx::named_bar_sync(1, kTauMath);
-      const int ncb = s_ncb;
       for (int t = 0; t < n_iter; ++t) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-        for (int c = 0; c < ncb; ++c) {
-          float s[64];
-          read_tile(cblk[c], s);
+        for (int j = 0; j < nkb; ++j) {
+          float s[32];
+          read_tile(j, s);
+          float cm = fmaxf(s[0], s[31]);
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            float cm = s[32 * q];
+          for (int e = 1; e < 31; e += 2) cm = fmax3(cm, s[e], s[e + 1]);
+          if (__any_sync(0xffffffffu, fmaf(cm, ap.cp, -rs.tau) > 0.f)) {
 #pragma unroll
-            for (int e = 1; e < 32; e += 2) cm = fmax3(cm, s[32 * q + e], s[32 * q + e + 1]);
-            if (__any_sync(0xffffffffu, fmaf(cm, ap.cp, -rs.tau) > 0.f)) {
-#pragma unroll
-              for (int e = 0; e < 32; ++e) accum_f<E>(fmaf(s[32 * q + e], ap.cp, -rs.tau), ap, a0, a1, a2);
-            }
+            for (int e = 0; e < 32; ++e) accum_f<E>(fmaf(s[e], ap.cp, -rs.tau), ap, a0, a1, a2);
           }
         }
-        // combine the two column halves in a fixed order (identical update in both threads)
-        ptx::named_bar_sync(1, kTauMath);
-        xch[tid] = a0;
-        xch[kTauMath + tid] = a1;
-        xch[2 * kTauMath + tid] = a2;
-        ptx::named_bar_sync(1, kTauMath);
-        a0 = xch[r] + xch[128 + r];
-        a1 = xch[kTauMath + r] + xch[kTauMath + 128 + r];
-        a2 = xch[2 * kTauMath + r] + xch[2 * kTauMath + 128 + r];
+        row_sum3(a0, a1, a2);
         alg1_update(rs, a0, a1, a2, ap);
       }
-      if (hf == 0 && valid) tau_out[(long long)bh * g.N + row] = rs.tau;
+      if (qc == 0 && valid) tau_out[(long long)bh * g.N + row] = rs.tau;
     }
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();   // no CTA leaves while its peer may still multicast into it
-  if (warp == 9) ptx::tmem_dealloc<128 * kTauSBuf>(tmem);
+  if (warp == kTauMathWarps + 1) ptx::tmem_dealloc<128 * kTauSBuf>(tmem);
 }
 
 }  // namespace sm100

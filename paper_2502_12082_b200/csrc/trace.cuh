@@ -14,7 +14,12 @@ extern __device__ int g_trace_bx;
     if (blockIdx.x == (unsigned)::entmax::g_trace_bx && blockIdx.y == 0 && (slot) < 8192)       \
       ::entmax::g_trace[(slot)] = clock64();                                                  \
   } while (0)
+// count an event over all CTAs (slots 8100..8191)
+#define ENTMAX_TRACE_COUNT(slot) atomicAdd(&::entmax::g_trace[(slot)], 1ull)
 #else
+#define ENTMAX_TRACE_COUNT(slot) \
+  do {                           \
+  } while (0)
 #define ENTMAX_TRACE_EV(slot) \
   do {                        \
   } while (0)

@@ -22,6 +22,9 @@ any code.  Recipes (DESIGN.md §"Input recipe"):
   Keys keep a Gaussian spread around their cluster direction (a near-constant
   key set would make dQ = Σ dS·K a near-total cancellation).
 
+* ``step``      — Gaussian with the first half of the keys scaled by 0.2 (structure test for the
+  τ kernel's list-overflow tiers; no paper workload).
+
 Every head (b, h) is drawn from its own stream seeded by (seed, b, h), so a rank
 that owns a slice of heads regenerates exactly its slice.
 Arrays are float32 numpy; callers round to the kernel dtype (bf16 RN via torch)
@@ -31,7 +34,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["head_rng", "gaussian_head", "planted_head", "make_inputs", "HeadSpec"]
+__all__ = ["head_rng", "gaussian_head", "planted_head", "step_head", "make_inputs", "HeadSpec"]
 
 
 def head_rng(seed: int, b: int, h: int, stream: int = 0) -> np.random.Generator:
@@ -90,6 +93,15 @@ def planted_head(N: int, d: int, rho: float, seed: int, b: int = 0, h: int = 0,
     return f32(q), f32(k), f32(v), f32(do), owned
 
 
+def step_head(N: int, d: int, seed: int, b: int = 0, h: int = 0, sigma2_q: float = 6.0, low: float = 0.2):
+    """Gaussian head whose first ⌊N/2⌋ keys are scaled by ``low``: their scores are bunched far below
+    the row maxima, which all sit in the second half.  A structure test for streaming τ solvers
+    that filter against a running maximum (the early keys all pass the early thresholds)."""
+    q, k, v, do = gaussian_head(N, d, seed, b, h, sigma2_q)
+    k[: N // 2] *= np.float32(low)
+    return q, k, v, do
+
+
 class HeadSpec:
     """Plain description of one generated workload."""
 
@@ -102,6 +114,8 @@ class HeadSpec:
             return gaussian_head(N, d, seed, b, h, self.sigma2_q)
         if self.kind == "planted":
             return planted_head(N, d, self.rho, seed, b, h, self.Br, self.Bc)[:4]
+        if self.kind == "step":
+            return step_head(N, d, seed, b, h, self.sigma2_q)
         raise ValueError(f"unknown generator kind {self.kind!r}")
 
 

@@ -104,11 +104,23 @@ def test_deterministic_and_head_sharding_bitwise():
     (4096, 1.25, 6.0, False),   # small α: wide candidate set
 ])
 def test_parity_candidate_overflow_fallback(N, alpha, sigma2, causal):
-    """Rows whose candidate list (z > τ_lo) overflows shared memory take the streaming Alg. 3
-    fallback inside the τ kernel; results must be identical in quality."""
+    """Rows whose candidate list (z > τ_lo) overflows shared memory even at the exact threshold
+    take the streaming Alg. 3 passes (tier 2) inside the τ kernel; results must be identical in
+    quality."""
     _require_gpu()
     spec = synth.HeadSpec("gaussian", sigma2_q=sigma2)
     dev, ref = make_case(1, 2, N, 64, torch.bfloat16, seed=9, spec=spec)
     fw, grads = run_gpu(dev, alpha, causal, 3)
     for bh in range(2):
         check_head(fw, ref, bh, alpha, causal, 3, torch.bfloat16, grads=grads)
+
+
+@pytest.mark.parametrize("N,causal", [(2048, False), (2304, True)])
+def test_parity_transient_overflow_rebuild(N, causal):
+    """`step` heads: every early key passes the running threshold, so the one-pass lists overflow;
+    the exact-threshold rebuild pass (tier 1) holds the final candidates."""
+    _require_gpu()
+    dev, ref = make_case(1, 2, N, 64, torch.bfloat16, seed=13, spec=synth.HeadSpec("step"))
+    fw, grads = run_gpu(dev, 1.5, causal, 3)
+    for bh in range(2):
+        check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
