@@ -4,7 +4,7 @@ ARCH   := -gencode arch=compute_100a,code=sm_100a
 CFLAGS := -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall -Iinclude -Ipaper_2502_12082_b200/csrc \
           --expt-relaxed-constexpr
 SRC    := paper_2502_12082_b200/csrc
-OBJS   := build/entmax_attn.o build/simt.o build/sm100.o
+OBJS   := build/entmax_attn.o build/simt.o build/sm100.o build/rowwise.o
 LIB    := paper_2502_12082_b200/libentmax_attn.so
 
 PROBE  := tests/probe/libprobe.so

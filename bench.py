@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--sweep", action="store_true", help="add the planted block-sparsity sweep")
+    ap.add_argument("--suite", action="store_true", help="add configs 3-5 (seq-len / alpha / long-context lines)")
+    ap.add_argument("--no-rowwise", action="store_true", help="skip the standalone row-wise solver line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--N", type=int, default=CFG["N"])
     ap.add_argument("--d", type=int, default=CFG["d"])
@@ -355,6 +357,10 @@ def main():
 
     if args.sweep and rank == 0:
         line["sweep"] = run_sweep(P, synth, torch, dev, cfg, args)
+    if args.suite and rank == 0:
+        line["suite"] = run_suite(P, synth, torch, dev, args)
+    if not args.no_rowwise and rank == 0:
+        line["next1_rowwise"] = run_rowwise(P, synth, torch, dev, peaks)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, fl, desc = oracle_sample(dict(cfg), seed=0, rows=4096)
@@ -406,6 +412,85 @@ def run_sweep(P, synth, torch, dev, cfg, args):
                     "eff_tflops_fwd_bwd": 14.0 * d * pairs / (res["fwd_bwd"] * 1e-3) / 1e12,
                     **({"sdpa_fwd_bwd_ms": sd} if sd else {})})
         del q, k, v, do, fw, g
+    return out
+
+
+def _time(torch, fn, iters):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def run_rowwise(P, synth, torch, dev, peaks, rows=8192, n=8192):
+    """the paper's standalone solver benchmark (Gaussian rows,
+    n = 8192, Halley-bisection T = 3 vs bisection; paper H100: 2.38 ms vs 36.67 ms).  HBM-bound:
+    algorithmic bytes = one read of s + one write of p (+ τ) per call; roofline against the
+    measured burst copy bandwidth (the kernel is timed alone)."""
+    s_np, dp_np = synth.rowwise_scores(rows, n, seed=0)
+    out = {"workload": f"[{rows} x {n}] s~N(0,1) (P:L246), alpha=1.5", "paper_h100_ms":
+           {"halley_bisection_T3": 2.38, "torch_bisection": 36.67}}
+    for dt_name, dt in (("f32", torch.float32), ("bf16", torch.bfloat16)):
+        s = torch.from_numpy(s_np).to(dt).to(dev)
+        dp = torch.from_numpy(dp_np).to(dt).to(dev)
+        esz = s.element_size()
+        byt = rows * n * esz * 2 + rows * 4
+        p, _ = P.entmax_rowwise_fwd(s, 1.5, 3)
+        P.profile_reset()
+        P.profile_enable(True)
+        ms_h = _time(torch, lambda: P.entmax_rowwise_fwd(s, 1.5, 3), 20)
+        P.profile_enable(False)
+        prof = P.profile_collect()
+        k_ms = prof["rowwise_fwd"][1] / prof["rowwise_fwd"][0]
+        ms_b = _time(torch, lambda: P.entmax_rowwise_fwd(s, 1.5, 23, halley=False), 20)
+        ms_bwd = _time(torch, lambda: P.entmax_rowwise_bwd(p, dp, 1.5), 20)
+        ach = byt / (k_ms * 1e-3) / 1e9
+        out[dt_name] = {
+            "halley_T3_ms": ms_h, "bisection_T23_ms": ms_b, "bwd_ms": ms_bwd,
+            "roofline": {"kernel": "rowwise_fwd", "bound": "hbm", "achieved": ach, "peak": peaks["hbm"],
+                         "unit": "GB/s", "frac": ach / peaks["hbm"], "traffic": None,
+                         "algorithmic": f"{byt} B/launch (read s + write p + tau)"},
+            "bwd_gbs": (rows * n * esz * 3) / (ms_bwd * 1e-3) / 1e9}
+        del s, dp, p
+    return out
+
+
+def run_suite(P, synth, torch, dev, args):
+    """BASELINE.json configs 3-5 (one line each): fwd and fwd+bwd ms and effective TFLOP/s."""
+    cases = [("config3", 8, 12, 512, 64, 1.5, False), ("config3", 8, 12, 8192, 64, 1.5, False),
+             ("config4", 8, 12, 1024, 64, 1.25, True), ("config4", 8, 12, 1024, 64, 1.5, True),
+             ("config4", 8, 12, 1024, 64, 2.0, True),
+             ("config5", 1, 16, 32768, 128, 1.5, True), ("config5", 1, 16, 65536, 128, 1.5, True)]
+    out = []
+    for name, B, H, N, d, alpha, causal in cases:
+        qn, kn, vn, don = synth.make_inputs(B, H, N, d, seed=99, spec=synth.HeadSpec("gaussian"))
+        q, k, v, do = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in (qn, kn, vn, don)]
+        del qn, kn, vn, don
+        fw = P.entmax_attn_fwd(q, k, v, alpha, causal, 3)
+        g = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
+        it = 3 if N >= 32768 else 10
+        f_ms = _time(torch, lambda: P.entmax_attn_fwd(q, k, v, alpha, causal, 3, out=fw), it)
+
+        def fb():
+            P.entmax_attn_fwd(q, k, v, alpha, causal, 3, out=fw)
+            P.entmax_attn_bwd(q, k, v, do, fw, alpha, causal, grads=g)
+        fb_ms = _time(torch, fb, it)
+        pairs = visible_pairs_in_active_blocks(fw.mask, N, causal)
+        sd = sdpa_ms(torch, q, k, v, do, causal, iters=it)
+        out.append({"config": name, "B": B, "H": H, "N": N, "d": d, "alpha": alpha, "causal": causal,
+                    "block_density": pairs / (B * H * total_visible_pairs(N, causal)),
+                    "fwd_ms": f_ms, "fwd_bwd_ms": fb_ms,
+                    "eff_tflops_fwd": 4.0 * d * pairs / (f_ms * 1e-3) / 1e12,
+                    "eff_tflops_fwd_bwd": 14.0 * d * pairs / (fb_ms * 1e-3) / 1e12,
+                    "sdpa_fwd_bwd_ms": sd})
+        del q, k, v, do, fw, g
+        torch.cuda.empty_cache()
     return out
 
 

@@ -9,6 +9,9 @@ Public API (same names as the C ABI):
   entmax_attn_fwd(q, k, v, alpha, causal, n_iter, scale=None, training=True) -> FwdResult
   entmax_attn_bwd(q, k, v, d_o, fwd: FwdResult, alpha, causal, scale=None) -> (dq, dk, dv)
   entmax_attention(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None)  (autograd op)
+  entmax_rowwise_fwd(s, alpha, n_iter, halley=True) -> (p, tau)    (include/entmax_rowwise.h)
+  entmax_rowwise_bwd(p, dp, alpha) -> ds
+  entmax(s, alpha=1.5, n_iter=3, halley=True)  (autograd op over the last dimension)
 q, k, v: [B, H, N, d] CUDA tensors, bf16 (tcgen05 path) or fp32 (SIMT fp32 path), same
 strides, last dim contiguous.
 """
@@ -24,7 +27,7 @@ from ._lib import EntmaxAttnError, ENTMAX_BF16, ENTMAX_FP32
 
 __all__ = ["entmax_attn_fwd", "entmax_attn_bwd", "entmax_attention", "block_size", "FwdResult",
            "EntmaxAttnError", "impl_for", "profile_enable", "profile_reset", "profile_collect",
-           "workspace_bytes"]
+           "workspace_bytes", "entmax_rowwise_fwd", "entmax_rowwise_bwd", "entmax"]
 
 _DT = {torch.bfloat16: ENTMAX_BF16, torch.float32: ENTMAX_FP32}
 
@@ -178,3 +181,81 @@ def profile_collect():
     ms = (ctypes.c_double * cap)()
     n = _lib.lib().entmax_attn_profile_collect(names, launches, ms, cap)
     return {names[i].decode(): (launches[i], ms[i]) for i in range(n)}
+
+
+# ------------------------------------------------------------------------------------------
+# Standalone row-wise α-entmax (include/entmax_rowwise.h)
+# ------------------------------------------------------------------------------------------
+
+def _rows_view(x: torch.Tensor):
+    if not x.is_cuda:
+        raise RuntimeError("entmax_rowwise: tensors must be CUDA tensors (no CPU fallback)")
+    if x.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {x.dtype}")
+    if x.dim() < 1 or x.stride(-1) != 1:
+        raise ValueError("last dimension must be contiguous")
+    n = x.shape[-1]
+    x2 = x.reshape(-1, n)
+    if x2.stride(-1) != 1:
+        x2 = x2.contiguous()
+    return x2, x2.shape[0], n, x2.stride(0) if x2.shape[0] > 1 else n
+
+
+def _padded_rows(x2: torch.Tensor, rows: int, n: int):
+    """(tensor, ld) with a 16-byte-multiple leading dimension (copies only when needed)."""
+    q = 16 // x2.element_size()
+    ld = x2.stride(0) if rows > 1 else -(-n // q) * q
+    if ld % q == 0 and ld >= n:
+        return x2, ld
+    ldp = -(-n // q) * q
+    buf = torch.zeros((rows, ldp), dtype=x2.dtype, device=x2.device)
+    buf[:, :n] = x2
+    return buf[:, :n], ldp
+
+
+def entmax_rowwise_fwd(s: torch.Tensor, alpha=1.5, n_iter=3, halley=True):
+    """p = α-entmax(s) over the last dimension by T = n_iter Halley-bisection (Alg. 1) or
+    bisection (halley=False) iterations; returns (p, τ) with τ in the pre-scaled convention."""
+    s2, rows, n, _ = _rows_view(s)
+    s2, ld = _padded_rows(s2, rows, n)
+    p = torch.empty((rows, ld), dtype=s.dtype, device=s.device)
+    t = torch.empty(rows, dtype=torch.float32, device=s.device)
+    st = _lib.lib().entmax_rowwise_fwd(_ptr(s2), rows, n, ld, _DT[s.dtype], float(alpha), int(n_iter),
+                                       int(bool(halley)), _ptr(p), _ptr(t), _stream(s.device))
+    _lib.check(st, "entmax_rowwise_fwd")
+    return p[:, :n].reshape(s.shape), t.reshape(s.shape[:-1])
+
+
+def entmax_rowwise_bwd(p: torch.Tensor, dp: torch.Tensor, alpha=1.5):
+    """ds = u ⊙ dp − (⟨u, dp⟩/‖u‖₁)·u with u = p^{2−α}, over the last dimension."""
+    if dp.shape != p.shape or dp.dtype != p.dtype:
+        raise ValueError("p and dp must share shape and dtype")
+    p2, rows, n, _ = _rows_view(p.contiguous())
+    d2 = dp.contiguous().reshape(rows, n)
+    p2, ld = _padded_rows(p2, rows, n)
+    if ld != n:
+        d2, _ = _padded_rows(d2, rows, n)
+    ds = torch.empty((rows, ld), dtype=p.dtype, device=p.device)
+    st = _lib.lib().entmax_rowwise_bwd(_ptr(p2), _ptr(d2), rows, n, ld, _DT[p.dtype], float(alpha), _ptr(ds),
+                                       _stream(p.device))
+    _lib.check(st, "entmax_rowwise_bwd")
+    return ds[:, :n].reshape(p.shape)
+
+
+class _Entmax(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, s, alpha, n_iter, halley):
+        p, _ = entmax_rowwise_fwd(s.contiguous(), alpha, n_iter, halley)
+        ctx.save_for_backward(p)
+        ctx.alpha = alpha
+        return p
+
+    @staticmethod
+    def backward(ctx, dp):
+        (p,) = ctx.saved_tensors
+        return entmax_rowwise_bwd(p, dp.contiguous(), ctx.alpha), None, None, None
+
+
+def entmax(s, alpha=1.5, n_iter=3, halley=True):
+    """α-entmax over the last dimension (Eq. 2) by Halley-bisection (autograd op)."""
+    return _Entmax.apply(s, alpha, n_iter, halley)

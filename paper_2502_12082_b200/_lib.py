@@ -1,4 +1,5 @@
-"""ctypes loader for libentmax_attn.so (the C ABI declared in include/entmax_attn.h).
+"""ctypes loader for libentmax_attn.so (the C ABI declared in include/entmax_attn.h and
+include/entmax_rowwise.h).
 
 The library is built in-tree (``make`` at the repo root, or ``__graft_entry__.build()``).
 If it is missing or fails to load, every entry point raises: there is no fallback path.
@@ -66,6 +67,11 @@ def lib() -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_double), i32]
     L.entmax_attn_impl_for.restype = i32
     L.entmax_attn_impl_for.argtypes = [pshape, i32]
+    i64 = ctypes.c_int64
+    L.entmax_rowwise_fwd.restype = i32          # include/entmax_rowwise.h
+    L.entmax_rowwise_fwd.argtypes = [vp, i64, ctypes.c_int32, i64, i32, f32, i32, i32, vp, vp, vp]
+    L.entmax_rowwise_bwd.restype = i32
+    L.entmax_rowwise_bwd.argtypes = [vp, vp, i64, ctypes.c_int32, i64, i32, f32, vp, vp]
     _lib = L
     return L
 

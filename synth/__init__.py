@@ -34,7 +34,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["head_rng", "gaussian_head", "planted_head", "step_head", "make_inputs", "HeadSpec"]
+__all__ = ["head_rng", "gaussian_head", "planted_head", "step_head", "make_inputs", "HeadSpec", "rowwise_scores"]
 
 
 def head_rng(seed: int, b: int, h: int, stream: int = 0) -> np.random.Generator:
@@ -139,3 +139,13 @@ def make_inputs(B: int, H: int, N: int, d: int, seed: int, spec: HeadSpec | None
         for t, x in zip(out, spec.head(N, d, seed, b, h)):
             t[n_] = x
     return tuple(out)
+
+
+def rowwise_scores(rows: int, n: int, seed: int, sigma: float = 1.0, with_grad: bool = True):
+    """Inputs of the standalone row-wise solver benchmark ("random tensors from a standard
+    Gaussian distribution (μ = 0, σ² = 1) with a fixed sequence length of n = 8192"): s ~ N(0, σ²)
+    of shape (rows, n) float32, and an upstream gradient dp ~ N(0, 1) of the same shape."""
+    rng = head_rng(seed, 0, 0, stream=7)
+    s = rng.standard_normal((rows, n), dtype=np.float32) * np.float32(sigma)
+    dp = rng.standard_normal((rows, n), dtype=np.float32) if with_grad else None
+    return s, dp

@@ -9,20 +9,24 @@ import pytest
 from paper_2502_12082_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "entmax_attn.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in sorted(os.listdir(os.path.join(ROOT, "include")))
+           if h.endswith(".h")]
 
 
 def _declared():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(entmax_attn_\w+)\s*\(", src)))
+    names = set()
+    for h in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names |= set(re.findall(r"\b(entmax_\w+)\s*\(", src))
+    return sorted(names)
 
 
 def test_header_declares_the_boundary():
     names = _declared()
     for must in ("entmax_attn_fwd", "entmax_attn_bwd", "entmax_attn_block_size",
                  "entmax_attn_fwd_workspace_bytes", "entmax_attn_bwd_workspace_bytes",
-                 "entmax_attn_status_string", "entmax_attn_last_error"):
+                 "entmax_attn_status_string", "entmax_attn_last_error",
+                 "entmax_rowwise_fwd", "entmax_rowwise_bwd"):
         assert must in names
 
 
@@ -83,3 +87,21 @@ def test_binding_refuses_cpu_tensors():
     x = torch.zeros(1, 1, 128, 64, dtype=torch.bfloat16)
     with pytest.raises(RuntimeError):
         P.entmax_attn_fwd(x, x, x)
+
+
+@pytest.mark.parametrize("alpha,n_iter,rows,n,ld,status", [
+    (1.0, 3, 4, 64, 64, 1), (2.5, 3, 4, 64, 64, 2), (1.5, 0, 4, 64, 64, 1),
+    (1.5, 3, 0, 64, 64, 1), (1.5, 3, 4, 0, 64, 1), (1.5, 3, 4, 64, 32, 1), (1.5, 3, 4, 63, 63, 1)])
+def test_rowwise_rejects_bad_arguments_before_launch(alpha, n_iter, rows, n, ld, status):
+    L = _lib.lib()
+    fake = ctypes.c_void_p(0x10000)   # never dereferenced: validation fails first
+    rc = L.entmax_rowwise_fwd(fake, rows, n, ld, 1, alpha, n_iter, 1, fake, None, None)
+    assert rc == status
+    assert L.entmax_attn_last_error().decode()
+
+
+def test_rowwise_bwd_rejects_misaligned_pointer():
+    L = _lib.lib()
+    rc = L.entmax_rowwise_bwd(ctypes.c_void_p(0x10004), ctypes.c_void_p(0x10000), 2, 64, 64, 1, 1.5,
+                              ctypes.c_void_p(0x10000), None)
+    assert rc == 1
