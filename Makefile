@@ -18,10 +18,10 @@ trace: $(TRACE)
 trace-nold: tests/probe/libentmax_trace_nold.so
 
 tests/probe/libentmax_trace_nold.so: $(wildcard $(SRC)/*.cu $(SRC)/*.cuh $(SRC)/*.h) tests/probe/trace_api.cu
-	$(NVCC) $(ARCH) $(CFLAGS) -DENTMAX_TRACE -DENTMAX_TRACE_NOLD -rdc=true -shared -o $@ $(SRC)/entmax_attn.cu $(SRC)/simt.cu $(SRC)/sm100.cu tests/probe/trace_api.cu
+	$(NVCC) $(ARCH) $(CFLAGS) -DENTMAX_TRACE -DENTMAX_TRACE_NOLD -rdc=true -shared -o $@ $(SRC)/entmax_attn.cu $(SRC)/simt.cu $(SRC)/sm100.cu $(SRC)/rowwise.cu tests/probe/trace_api.cu
 
 $(TRACE): $(wildcard $(SRC)/*.cu $(SRC)/*.cuh $(SRC)/*.h) tests/probe/trace_api.cu
-	$(NVCC) $(ARCH) $(CFLAGS) -DENTMAX_TRACE -rdc=true -shared -o $@ $(SRC)/entmax_attn.cu $(SRC)/simt.cu $(SRC)/sm100.cu tests/probe/trace_api.cu
+	$(NVCC) $(ARCH) $(CFLAGS) -DENTMAX_TRACE -rdc=true -shared -o $@ $(SRC)/entmax_attn.cu $(SRC)/simt.cu $(SRC)/sm100.cu $(SRC)/rowwise.cu tests/probe/trace_api.cu
 
 $(PROBE): tests/probe/probe.cu $(SRC)/sm100_ptx.cuh $(SRC)/tmap.h
 	$(NVCC) $(ARCH) $(CFLAGS) -shared -o $@ $<

@@ -12,7 +12,10 @@
 // on the lists without recomputing S.  The same lists, tested against the final τ with the kernels'
 // own fma(s, c', −τ) > 0, give the exact block mask, so the output kernel only visits active blocks.
 // The first W blocks only raise the running max and are streamed again at the end (fewer transient
-// candidates).  Overflow (a row list is finite): tier 1 streams K once more with the exact threshold
+// candidates).  Each row list is split into four private quarters, one per thread of the row, so an
+// append is a plain shared store at a register counter (no atomics) and every thread's list keeps
+// the stream order: the iteration sums are formed in a fixed order and are bitwise reproducible
+// (entries appended under a racy, lower running threshold are <= τ_lo(m) and add exact zeros).  Overflow (a row list is finite): tier 1 streams K once more with the exact threshold
 // τ_lo(m); tier 2, if even that overflows (wide supports, small α), streams T more passes over all
 // visible blocks — Alg. 3 itself.
 // Warp roles (576 threads): warps 0-15 math (thread t: row t & 127, column quarter t >> 7 of each
@@ -37,22 +40,18 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return d;
 }
 
-// Row-list append: if v > thr, take slot = cnt++ (shared atomic; the row's four threads append
-// concurrently) and store (v, tag) there when slot < cap.  Lists are slot-major: [slot][128 rows];
-// tag = key block << 2 | column quarter of the appending thread.
-__device__ __forceinline__ void row_append(uint32_t cnt_addr, uint32_t ls_row, uint32_t lj_row, float v, float thr,
-                                           uint32_t tag, uint32_t cap) {
+// Private-list append: if v > thr, store v at [as] and the u16 tag at [aj] (only while as < end) and
+// advance both by one slot.  Lists are slot-major ([slot][128 rows]: 512 B per value slot, 256 B per
+// tag slot) so the lanes (rows) of a warp store to consecutive words; as keeps advancing past `end`
+// so the list length (and an overflow) is (as − start) / 512.
+__device__ __forceinline__ void list_append(uint32_t& as, uint32_t& aj, uint32_t end, float v, float thr,
+                                            uint32_t tag) {
   asm volatile(
-      "{\n\t.reg .pred q, w;\n\t.reg .u32 slot, a;\n\t"
-      "mov.u32 slot, 0;\n\t"
-      "setp.gt.f32 q, %3, %4;\n\t"
-      "@q atom.shared.add.u32 slot, [%0], 1;\n\t"
-      "setp.lt.and.u32 w, slot, %6, q;\n\t"
-      "mad.lo.u32 a, slot, 512, %1;\n\t"
-      "@w st.shared.f32 [a], %3;\n\t"
-      "mad.lo.u32 a, slot, 256, %2;\n\t"
-      "@w st.shared.u16 [a], %5;\n\t}" ::"r"(cnt_addr),
-      "r"(ls_row), "r"(lj_row), "f"(v), "f"(thr), "h"((unsigned short)tag), "r"(cap)
+      "{.reg .pred q, w;\n\tsetp.gt.f32 q, %2, %3;\n\tsetp.lt.and.u32 w, %0, %5, q;\n\t"
+      "@w st.shared.f32 [%0], %2;\n\t@w st.shared.u16 [%1], %4;\n\t"
+      "@q add.u32 %0, %0, 512;\n\t@q add.u32 %1, %1, 256;\n\t}"
+      : "+r"(as), "+r"(aj)
+      : "f"(v), "f"(thr), "h"((unsigned short)tag), "r"(end)
       : "memory");
 }
 
@@ -61,7 +60,8 @@ struct TauSmem {
   static constexpr int NST = (D == 64) ? 3 : 2;   // K-tile ring depth
   // list slots per row: the online pass appends ~37 scores per row on average for the paper's
   // Gaussian rows at N = 8192 (max ~140); the exact-threshold count has a heavy tail (DESIGN.md §τ)
-  static constexpr int CAP = (D == 64) ? 190 : 146;
+  static constexpr int CAP = (D == 64) ? 188 : 144;
+  static constexpr int CAPQ = CAP / 4;                                // private slots per thread
   static constexpr size_t tiles = (size_t)(1 + NST) * Cfg<D>::TILE;
   static constexpr size_t lists = (size_t)CAP * kBr * (4 + 2);     // score f32, key block u16
   static constexpr size_t fixed = 1024 + tiles + lists + 3 * kTauMath * 8 + 2 * kBr * 4;
@@ -82,6 +82,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   using SM = TauSmem<D>;
   constexpr int NST = SM::NST;
   constexpr int kCap = SM::CAP;
+  constexpr int kCapQ = SM::CAPQ;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
@@ -91,7 +92,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   float* xch = reinterpret_cast<float*>(list_j + kCap * kBr);               // [3][512] exchange (8-byte slots)
   uint64_t* xch64 = reinterpret_cast<uint64_t*>(xch);
   float* mshare = xch + 6 * kTauMath;                                        // [128] running row maxima
-  int* rowcnt = reinterpret_cast<int*>(mshare + kBr);                        // [128] list lengths
+  int* rowcnt = reinterpret_cast<int*>(mshare + kBr);                        // [128] (spare)
   uint8_t* cflag = reinterpret_cast<uint8_t*>(rowcnt + kBr);                 // [Tc] candidate blocks (τ_lo)
   uint8_t* aflag = cflag + g.Tc;                                             // [Tc] exact active blocks
   __shared__ __align__(8) uint64_t bar_q, k_full[NST], k_empty[NST], s_full[kTauSBuf], s_empty[kTauSBuf], dec_bar,
@@ -107,7 +108,10 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const int nkb = g.visible_kblocks(min((i | 1), g.Tr - 1));   // identical for both CTAs of the pair
   const long long li = (long long)bh * g.Tr + i;
   // warm-up: the first W blocks only raise the running max and are streamed again at the end
-  const int W = nkb >= 32 ? max(4, nkb / 8) : nkb / 8;
+#ifndef ENTMAX_TAU_WDIV
+#define ENTMAX_TAU_WDIV 8   // (diagnostics builds vary it)
+#endif
+  const int W = nkb >= 32 ? max(4, nkb / ENTMAX_TAU_WDIV) : nkb / ENTMAX_TAU_WDIV;
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
@@ -128,10 +132,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     cflag[j] = 0;
     aflag[j] = 0;
   }
-  if (threadIdx.x < kBr) {
-    mshare[threadIdx.x] = -INFINITY;
-    rowcnt[threadIdx.x] = 0;
-  }
+  if (threadIdx.x < kBr) mshare[threadIdx.x] = -INFINITY;
   if (warp == kTauMathWarps + 1) ptx::tmem_alloc<128 * kTauSBuf>(&tmem_base_sh);
   ptx::tc_fence_before();
   ptx::cluster_sync();   // both CTAs' barriers exist before any multicast targets them
@@ -261,22 +262,11 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
            (xch[2 * kTauMath + 256 + r] + xch[2 * kTauMath + 384 + r]);
     };
 
-    // the same for 64-bit fixed-point partial sums (integer adds: the combined sum is exact)
-    auto row_sum3_fx = [&](uint64_t& a0, uint64_t& a1, uint64_t& a2) {
-      ptx::named_bar_sync(1, kTauMath);
-      xch64[tid] = a0;
-      xch64[kTauMath + tid] = a1;
-      xch64[2 * kTauMath + tid] = a2;
-      ptx::named_bar_sync(1, kTauMath);
-      a0 = xch64[r] + xch64[128 + r] + xch64[256 + r] + xch64[384 + r];
-      a1 = xch64[kTauMath + r] + xch64[kTauMath + 128 + r] + xch64[kTauMath + 256 + r] + xch64[kTauMath + 384 + r];
-      a2 = xch64[2 * kTauMath + r] + xch64[2 * kTauMath + 128 + r] + xch64[2 * kTauMath + 256 + r] +
-           xch64[2 * kTauMath + 384 + r];
-    };
-
-    const uint32_t ls_row = ptx::smem_u32(list_s) + r * 4;     // slot c at + c·512
-    const uint32_t lj_row = ptx::smem_u32(list_j) + r * 2;     // slot c at + c·256
-    const uint32_t cnt_addr = ptx::smem_u32(rowcnt) + r * 4;
+    // this thread's private list: slots [qc·kCapQ, (qc+1)·kCapQ) of row r
+    const uint32_t ls0 = ptx::smem_u32(list_s) + (uint32_t)(qc * kCapQ) * 512u + r * 4;
+    const uint32_t lj0 = ptx::smem_u32(list_j) + (uint32_t)(qc * kCapQ) * 256u + r * 2;
+    const uint32_t ls_end = ls0 + (uint32_t)kCapQ * 512u;
+    uint32_t as = ls0, aj = lj0;
     const uint32_t msh = ptx::smem_u32(mshare) + r * 4;
     const float inv_cp = 1.0f / ap.cp;    // (the 3e-6 margin dwarfs the product's rounding)
     // conservative score threshold: s <= thr(m) ⇒ fma(s, c', −τ_lo(m)) <= 0 (margin >> fma rounding)
@@ -285,7 +275,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       return valid ? (lo - fmaxf(fabsf(lo), 1e-6f) * 3.0e-6f) * inv_cp : INFINITY;
     };
 
-    // One streaming pass appending the scores above the threshold to the row lists.
+    // One streaming pass appending the scores above the threshold to the thread's private list.
     // online: the threshold follows the running max of the row (own quarter + the row's published
     // value: a benign race, any value read is a lower bound of m); the first W blocks only raise
     // the max and are appended when they stream again at the end.  !online: fixed threshold `thr`.
@@ -294,6 +284,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       const int nsteps = online ? nkb + W : nkb;
       for (int t = 0; t < nsteps; ++t) {
         const int j = t < nkb ? t : t - nkb;
+        const float mread = online ? ptx::ld_shared_f32(msh) : 0.f;   // issued early (latency)
         float s[32];
         read_tile(j, s);
         float gm[4];
@@ -304,7 +295,6 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         }
         if (online && t < nkb) {
           const float tmax = fmax3(fmaxf(gm[0], gm[1]), gm[2], gm[3]);
-          const float mread = ptx::ld_shared_f32(msh);
           const float mnew = fmax3(mrun, tmax, mread);
           if (mnew > mrun) {
             mrun = mnew;
@@ -317,9 +307,12 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 #pragma unroll
         for (int gq = 0; gq < 4; ++gq) bits |= (gm[gq] > thr) ? (1u << gq) : 0u;
         const uint32_t wbits = __reduce_or_sync(0xffffffffu, bits);
+#ifdef ENTMAX_TAU_NOAPPEND
+        if (wbits != 0xdeadbeef) continue;   // diagnostics: timing of the common path only
+#endif
         if (wbits == 0) continue;
         if (lane == 0) cflag[j] = 1;    // τ_lo candidate block (a superset when online)
-        const uint32_t tag = ((uint32_t)j << 2) | (uint32_t)qc;
+        const uint32_t tag = (uint32_t)j;
         // groups of 8 keys with a candidate in some lane: warp-uniform branch.  A lane with one hit
         // in the group appends the group max; the per-key path runs only when some lane's
         // second-largest key of the group is a hit too.
@@ -337,13 +330,14 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
           const float m2 = fmax3(fminf(fmaxf(hh[0], hh[1]), fmaxf(hh[2], hh[3])), l01, l23);
           if (__any_sync(0xffffffffu, m2 > thr)) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) row_append(cnt_addr, ls_row, lj_row, sg[e], thr, tag, kCap);
+            for (int e = 0; e < 8; ++e) list_append(as, aj, ls_end, sg[e], thr, tag);
           } else {
-            row_append(cnt_addr, ls_row, lj_row, gm[gq], thr, tag, kCap);
+            list_append(as, aj, ls_end, gm[gq], thr, tag);
           }
         }
       }
     };
+    auto list_len = [&]() { return (int)((as - ls0) >> 9); };
 
     stream_pass(true);
     // row max m (Alg. 1 line 4) and bracket
@@ -353,7 +347,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const float n_vis = g.causal ? (float)(row + 1) : (float)g.N;
     RowState rs = bracket_init(smax * ap.cp, n_vis, ap.alpha);
     thr = thr_of(smax);
-    if (qc == 0 && rowcnt[r] > kCap) s_overflow = 1;
+    if (list_len() > kCapQ) s_overflow = 1;
     bool fallback = pair_any(0);
     if (tid == 0 && fallback) ENTMAX_TRACE_COUNT(8100);
     if (tid == 0) ENTMAX_TRACE_COUNT(8102);
@@ -363,55 +357,32 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         ptx::mbar_arrive(&dec_bar);
         s_overflow = 0;
       }
-      if (qc == 0) rowcnt[r] = 0;
+      as = ls0;
+      aj = lj0;
       ptx::named_bar_sync(1, kTauMath);
       stream_pass(false);
-      ptx::named_bar_sync(1, kTauMath);
-      if (qc == 0 && rowcnt[r] > kCap) s_overflow = 1;
+      if (list_len() > kCapQ) s_overflow = 1;
       fallback = pair_any(1);
       if (tid == 0 && fallback) ENTMAX_TRACE_COUNT(8101);
     }
 
     if (!fallback) {
-      // ---- T iterations of Alg. 1 on the row lists.  The list order depends on how the row's four
-      // threads' atomics interleaved, so the sums are formed order-independently:
-      //  E ∈ {1, 2, 4}: every term [x]_+^p (p = e, e−1, e−2 >= 0) lies in [0, 1] (x <= m·c' − τ_lo = 1),
-      //    so each thread sums a strided quarter of the list in 64-bit fixed point (2^-32 units; the
-      //    rounding is far below fp32 summation error) and the integer partial sums add exactly;
-      //  generic α: each thread sums the entries it appended (tag & 3) in its own append order —
-      //    its successive slot grabs are increasing — and the quarters combine in a fixed order.
-      // Either way the result is bitwise reproducible.
-      const int n = rowcnt[r];
+      // ---- T iterations of Alg. 1 on the row lists: each thread sums its own list in stream order
+      // and the row's four quarters combine in a fixed order (row_sum3), so τ is bitwise reproducible.
+      const int n = list_len();
       for (int t = 0; t < n_iter; ++t) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-        if constexpr (E != 0) {
-          uint64_t q0 = 0, q1 = 0, q2 = 0;
-          for (int c = qc; c < n; c += 4) {
-            float t0 = 0.f, t1 = 0.f, t2 = 0.f;
-            accum_f<E>(fmaf(ptx::ld_shared_f32(ls_row + c * 512), ap.cp, -rs.tau), ap, t0, t1, t2);
-            q0 += __float2ull_rn(t0 * 4294967296.0f);
-            q1 += __float2ull_rn(t1 * 4294967296.0f);
-            q2 += __float2ull_rn(t2 * 4294967296.0f);
-          }
-          row_sum3_fx(q0, q1, q2);
-          a0 = (float)q0 * 2.3283064365386963e-10f;
-          a1 = (float)q1 * 2.3283064365386963e-10f;
-          a2 = (float)q2 * 2.3283064365386963e-10f;
-        } else {
-          for (int c = 0; c < n; ++c) {
-            const bool mine = (ptx::ld_shared_u16(lj_row + c * 256) & 3u) == (uint32_t)qc;
-            const float x = fmaf(ptx::ld_shared_f32(ls_row + c * 512), ap.cp, -rs.tau);
-            accum_f<E>(mine ? x : -INFINITY, ap, a0, a1, a2);
-          }
-          row_sum3(a0, a1, a2);
-        }
+        for (int c = 0; c < n; ++c)
+          accum_f<E>(fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau), ap, a0, a1, a2);
+        row_sum3(a0, a1, a2);
         alg1_update(rs, a0, a1, a2, ap);
       }
       if (valid) {
         if (qc == 0) tau_out[(long long)bh * g.N + row] = rs.tau;
         // exact block activity from the final τ (same fma test as the output kernel)
-        for (int c = qc; c < n; c += 4)
-          if (fmaf(ptx::ld_shared_f32(ls_row + c * 512), ap.cp, -rs.tau) > 0.f) aflag[ptx::ld_shared_u16(lj_row + c * 256) >> 2] = 1;
+        for (int c = 0; c < n; ++c)
+          if (fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau) > 0.f)
+            aflag[ptx::ld_shared_u16(lj0 + (uint32_t)c * 256u)] = 1;
       }
       ptx::named_bar_sync(1, kTauMath);
       if (warp == 0 && real_cta) {
