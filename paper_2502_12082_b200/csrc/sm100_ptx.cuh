@@ -383,6 +383,12 @@ __device__ __forceinline__ float2 ld_shared_f2(uint32_t saddr) {
 __device__ __forceinline__ void st_shared_f32(uint32_t saddr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
 }
+__device__ __forceinline__ void st_shared_u16(uint32_t saddr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(saddr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void st_shared_u8(uint32_t saddr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(saddr), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ float ld_shared_f32(uint32_t saddr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr) : "memory");

@@ -18,9 +18,11 @@
 // (entries appended under a racy, lower running threshold are <= τ_lo(m) and add exact zeros).  Overflow (a row list is finite): tier 1 streams K once more with the exact threshold
 // τ_lo(m); tier 2, if even that overflows (wide supports, small α), streams T more passes over all
 // visible blocks — Alg. 3 itself.
-// Warp roles (576 threads): warps 0-15 math (thread t: row t & 127, column quarter t >> 7 of each
-// 128-key tile; warp w reads TMEM lanes 32·(w & 3)) — four warps per SM sub-partition hide the
-// latency of the short compare/branch chains; warp 16 TMA producer, warp 17 MMA issuer.
+// Warp roles (576 threads): warps 0-15 math in four groups of four (thread t: row t & 127; group
+// t >> 7 owns S buffer t >> 7 and processes every fourth tile of the stream, all 128 columns of it in
+// four 32-column TMEM loads; warp w reads TMEM lanes 32·(w & 3)), so four tiles are in processing at
+// once and a warp's per-tile overheads cover a whole row segment; warp 16 TMA producer, warp 17 MMA
+// issuer.
 #pragma once
 
 #include "sm100_kernels.cuh"
@@ -90,7 +92,6 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   float* list_s = reinterpret_cast<float*>(sK + NST * C::TILE);            // [CAP][128] scores
   uint16_t* list_j = reinterpret_cast<uint16_t*>(list_s + kCap * kBr);      // [CAP][128] key block
   float* xch = reinterpret_cast<float*>(list_j + kCap * kBr);               // [3][512] exchange (8-byte slots)
-  uint64_t* xch64 = reinterpret_cast<uint64_t*>(xch);
   float* mshare = xch + 6 * kTauMath;                                        // [128] running row maxima
   int* rowcnt = reinterpret_cast<int*>(mshare + kBr);                        // [128] (spare)
   uint8_t* cflag = reinterpret_cast<uint8_t*>(rowcnt + kBr);                 // [Tc] candidate blocks (τ_lo)
@@ -109,7 +110,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const long long li = (long long)bh * g.Tr + i;
   // warm-up: the first W blocks only raise the running max and are streamed again at the end
 #ifndef ENTMAX_TAU_WDIV
-#define ENTMAX_TAU_WDIV 8   // (diagnostics builds vary it)
+#define ENTMAX_TAU_WDIV 4   // (diagnostics builds vary it; 4 measured best of 2, 4, 8)
 #endif
   const int W = nkb >= 32 ? max(4, nkb / ENTMAX_TAU_WDIV) : nkb / ENTMAX_TAU_WDIV;
 
@@ -121,7 +122,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
     for (int s = 0; s < kTauSBuf; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&s_empty[s], kTauMathWarps);
+      ptx::mbar_init(&s_empty[s], kTauMathWarps / kTauSBuf);   // the 4 warps of one group
     }
     ptx::mbar_init(&dec_bar, 1);
     ptx::mbar_init(&x_bar, 1);
@@ -133,6 +134,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     aflag[j] = 0;
   }
   if (threadIdx.x < kBr) mshare[threadIdx.x] = -INFINITY;
+  if (threadIdx.x == 0) ENTMAX_TRACE_EV(8000);
   if (warp == kTauMathWarps + 1) ptx::tmem_alloc<128 * kTauSBuf>(&tmem_base_sh);
   ptx::tc_fence_before();
   ptx::cluster_sync();   // both CTAs' barriers exist before any multicast targets them
@@ -199,39 +201,48 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const bool valid = row < g.N;
     const int my_last = g.causal ? row : g.N - 1;
     const int cta_last = g.causal ? i * kBr : g.N - 1;
-    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + qc * 32;
-    int k = 0;
-    const uint32_t sfull0 = ptx::smem_u32(&s_full[0]), sempty0 = ptx::smem_u32(&s_empty[0]);
+    // Work split: warp group qc (warps 4qc..4qc+3, one per TMEM lane quadrant) owns S buffer qc and
+    // processes every tile whose global stream index k satisfies k % 4 == qc, all 128 columns of it
+    // in four 32-column chunks.  The four groups work on four different tiles at once, so the MMA
+    // for tile k+4 waits only on group qc, and a warp's per-tile overheads cover 128 columns.
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16) + qc * 128;
+    int kglob = 0;   // global stream index of the next pass's first tile (the MMA issuer's order)
+    const uint32_t sfull = ptx::smem_u32(&s_full[qc]), sempty = ptx::smem_u32(&s_empty[qc]);
 
-    // read this thread's 32 scores of step k (columns qc*32 .. +31 of key block j), masked
-    auto read_tile = [&](int j, float (&s)[32]) {
-      const int sb = k % kTauSBuf;
-      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k);
-      ptx::mbar_wait_addr(sfull0 + 8 * sb, (k / kTauSBuf) & 1);
-      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k + 1);
+    auto wait_tile = [&](int kk) {
+      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * (kk >> 2));
+      ptx::mbar_wait_addr(sfull, (kk >> 2) & 1);
+      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * (kk >> 2) + 1);
       ptx::tc_fence_after();
+    };
+    // chunk c (columns 32c .. 32c+31 of key block j) of the waited tile, masked; the last chunk's
+    // load releases the S buffer to the MMA issuer
+    auto read_chunk = [&](int j, int c, float (&s)[32]) {
       uint32_t ra[32];
 #ifdef ENTMAX_TRACE_NOLD
 #pragma unroll
       for (int e = 0; e < 32; ++e) ra[e] = 0u;
 #else
-      ptx::tmem_ld32(lane_base + sb * 128, ra);
+      ptx::tmem_ld32(lane_base + c * 32, ra);
       ptx::tmem_wait_ld();
 #endif
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_addr(sempty0 + 8 * sb);
-      if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * k + 2);
+      if (c == 3) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_addr(sempty);
+        if (threadIdx.x == 0) ENTMAX_TRACE_EV(3072 + 3 * (j >> 2) + 2);
+      }
 #pragma unroll
       for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(ra[e]);
       if ((j + 1) * kBc - 1 > cta_last) {
-        const int key0 = j * kBc + qc * 32;
+        const int key0 = j * kBc + c * 32;
 #pragma unroll
         for (int e = 0; e < 32; ++e)
           if (key0 + e > my_last) s[e] = -INFINITY;
       }
-      ++k;
     };
+    // first step t >= 0 of a pass starting at global index k0 that belongs to this group
+    auto first_t = [&](int k0) { return (qc - k0 % kTauSBuf + kTauSBuf) % kTauSBuf; };
 
     // the two CTAs of the pair stream the same K blocks, so every fallback decision is joint
     // (s_overflow is read after the barrier: every thread's write to it must be visible)
@@ -268,6 +279,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const uint32_t ls_end = ls0 + (uint32_t)kCapQ * 512u;
     uint32_t as = ls0, aj = lj0;
     const uint32_t msh = ptx::smem_u32(mshare) + r * 4;
+    const uint32_t cflag_s = ptx::smem_u32(cflag);
     const float inv_cp = 1.0f / ap.cp;    // (the 3e-6 margin dwarfs the product's rounding)
     // conservative score threshold: s <= thr(m) ⇒ fma(s, c', −τ_lo(m)) <= 0 (margin >> fma rounding)
     auto thr_of = [&](float m) {
@@ -282,64 +294,68 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     float mrun = -INFINITY, thr = thr_of(-INFINITY);
     auto stream_pass = [&](bool online) {
       const int nsteps = online ? nkb + W : nkb;
-      for (int t = 0; t < nsteps; ++t) {
+      for (int t = first_t(kglob); t < nsteps; t += kTauSBuf) {
         const int j = t < nkb ? t : t - nkb;
-        const float mread = online ? ptx::ld_shared_f32(msh) : 0.f;   // issued early (latency)
-        float s[32];
-        read_tile(j, s);
-        float gm[4];
+        wait_tile(kglob + t);
+        const float mread = online ? ptx::ld_shared_f32(msh) : 0.f;   // once per tile
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float s[32];
+          read_chunk(j, c, s);
+          float gm[4];
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) {
-          const float* sg = s + 8 * gq;
-          gm[gq] = fmax3(fmax3(sg[0], sg[1], sg[2]), fmax3(sg[3], sg[4], sg[5]), fmaxf(sg[6], sg[7]));
-        }
-        if (online && t < nkb) {
-          const float tmax = fmax3(fmaxf(gm[0], gm[1]), gm[2], gm[3]);
-          const float mnew = fmax3(mrun, tmax, mread);
-          if (mnew > mrun) {
-            mrun = mnew;
-            thr = thr_of(mrun);
+          for (int gq = 0; gq < 4; ++gq) {
+            const float* sg = s + 8 * gq;
+            gm[gq] = fmax3(fmax3(sg[0], sg[1], sg[2]), fmax3(sg[3], sg[4], sg[5]), fmaxf(sg[6], sg[7]));
           }
-          if (tmax > mread) ptx::st_shared_f32(msh, mrun);
-          if (t < W) continue;
-        }
-        uint32_t bits = 0;
+          if (online && t < nkb) {
+            const float tmax = fmax3(fmaxf(gm[0], gm[1]), gm[2], gm[3]);
+            if (tmax > mread) ptx::st_shared_f32(msh, fmaxf(tmax, mrun));
+            mrun = fmax3(mrun, tmax, mread);
+            thr = thr_of(mrun);                 // branch-free (same value when mrun is unchanged)
+            if (t < W) continue;
+          }
+          bool hit[4];
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) bits |= (gm[gq] > thr) ? (1u << gq) : 0u;
-        const uint32_t wbits = __reduce_or_sync(0xffffffffu, bits);
+          for (int gq = 0; gq < 4; ++gq) hit[gq] = gm[gq] > thr;
 #ifdef ENTMAX_TAU_NOAPPEND
-        if (wbits != 0xdeadbeef) continue;   // diagnostics: timing of the common path only
+          if (thr != -12345.f) continue;   // diagnostics: timing of the common path only
 #endif
-        if (wbits == 0) continue;
-        if (lane == 0) cflag[j] = 1;    // τ_lo candidate block (a superset when online)
-        const uint32_t tag = (uint32_t)j;
-        // groups of 8 keys with a candidate in some lane: warp-uniform branch.  A lane with one hit
-        // in the group appends the group max; the per-key path runs only when some lane's
-        // second-largest key of the group is a hit too.
+          if (!__any_sync(0xffffffffu, (hit[0] | hit[1]) | (hit[2] | hit[3]))) continue;
+          if (lane == 0) ptx::st_shared_u8(cflag_s + j, 1);   // τ_lo candidate block (a superset when online)
+          const uint32_t tag = (uint32_t)j;
+          // groups of 8 keys with a candidate in some lane: warp-uniform branch.  A lane with one hit
+          // in the group appends the group max; the per-key path runs only when some lane's
+          // second-largest key of the group is a hit too.
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) {
-          if (!(wbits & (1u << gq))) continue;
-          const float* sg = s + 8 * gq;
-          float hh[4], ll[4];
+          for (int gq = 0; gq < 4; ++gq) {
+            if (!__any_sync(0xffffffffu, hit[gq])) continue;
+            const float* sg = s + 8 * gq;
+            float hh[4], ll[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            hh[q] = fmaxf(sg[2 * q], sg[2 * q + 1]);
-            ll[q] = fminf(sg[2 * q], sg[2 * q + 1]);
-          }
-          const float l01 = fmax3(fminf(hh[0], hh[1]), ll[0], ll[1]), l23 = fmax3(fminf(hh[2], hh[3]), ll[2], ll[3]);
-          const float m2 = fmax3(fminf(fmaxf(hh[0], hh[1]), fmaxf(hh[2], hh[3])), l01, l23);
-          if (__any_sync(0xffffffffu, m2 > thr)) {
+            for (int q = 0; q < 4; ++q) {
+              hh[q] = fmaxf(sg[2 * q], sg[2 * q + 1]);
+              ll[q] = fminf(sg[2 * q], sg[2 * q + 1]);
+            }
+            const float l01 = fmax3(fminf(hh[0], hh[1]), ll[0], ll[1]),
+                        l23 = fmax3(fminf(hh[2], hh[3]), ll[2], ll[3]);
+            const float m2 = fmax3(fminf(fmaxf(hh[0], hh[1]), fmaxf(hh[2], hh[3])), l01, l23);
+            if (__any_sync(0xffffffffu, m2 > thr)) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) list_append(as, aj, ls_end, sg[e], thr, tag);
-          } else {
-            list_append(as, aj, ls_end, gm[gq], thr, tag);
+              for (int e = 0; e < 8; ++e) list_append(as, aj, ls_end, sg[e], thr, tag);
+            } else {
+              list_append(as, aj, ls_end, gm[gq], thr, tag);
+            }
           }
         }
       }
+      kglob += nsteps;
     };
     auto list_len = [&]() { return (int)((as - ls0) >> 9); };
 
+    if (tid == 0) ENTMAX_TRACE_EV(8003);
     stream_pass(true);
+    if (tid == 0) ENTMAX_TRACE_EV(8004);
     // row max m (Alg. 1 line 4) and bracket
     xch[tid] = mrun;
     ptx::named_bar_sync(1, kTauMath);
@@ -369,6 +385,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     if (!fallback) {
       // ---- T iterations of Alg. 1 on the row lists: each thread sums its own list in stream order
       // and the row's four quarters combine in a fixed order (row_sum3), so τ is bitwise reproducible.
+      if (tid == 0) ENTMAX_TRACE_EV(8005);
       const int n = list_len();
       for (int t = 0; t < n_iter; ++t) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f;
@@ -377,6 +394,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         row_sum3(a0, a1, a2);
         alg1_update(rs, a0, a1, a2, ap);
       }
+      if (tid == 0) ENTMAX_TRACE_EV(8008);
       if (valid) {
         if (qc == 0) tau_out[(long long)bh * g.N + row] = rs.tau;
         // exact block activity from the final τ (same fma test as the output kernel)
@@ -384,11 +402,14 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
           if (fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau) > 0.f)
             aflag[ptx::ld_shared_u16(lj0 + (uint32_t)c * 256u)] = 1;
       }
+      if (tid == 0) ENTMAX_TRACE_EV(8009);
       ptx::named_bar_sync(1, kTauMath);
+      if (tid == 0) ENTMAX_TRACE_EV(8010);
       if (warp == 0 && real_cta) {
         const int nb = compact_flags(aflag, nkb, cand_idx + li * g.Tc);
         if (lane == 0) cand_cnt[li] = nb;
       }
+      if (tid == 0) ENTMAX_TRACE_EV(8011);
       if (tid == 0) {
         __threadfence_block();
         ptx::mbar_arrive(&dec_bar);
@@ -406,19 +427,24 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
           ptx::mbar_arrive(&dec_bar);
         }
       }
-      for (int t = 0; t < n_iter; ++t) {
+      for (int it = 0; it < n_iter; ++it) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-        for (int j = 0; j < nkb; ++j) {
-          float s[32];
-          read_tile(j, s);
-          float cm = fmaxf(s[0], s[31]);
+        for (int t = first_t(kglob); t < nkb; t += kTauSBuf) {
+          wait_tile(kglob + t);
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            float s[32];
+            read_chunk(t, c, s);
+            float cm = fmaxf(s[0], s[31]);
 #pragma unroll
-          for (int e = 1; e < 31; e += 2) cm = fmax3(cm, s[e], s[e + 1]);
-          if (__any_sync(0xffffffffu, fmaf(cm, ap.cp, -rs.tau) > 0.f)) {
+            for (int e = 1; e < 31; e += 2) cm = fmax3(cm, s[e], s[e + 1]);
+            if (__any_sync(0xffffffffu, fmaf(cm, ap.cp, -rs.tau) > 0.f)) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) accum_f<E>(fmaf(s[e], ap.cp, -rs.tau), ap, a0, a1, a2);
+              for (int e = 0; e < 32; ++e) accum_f<E>(fmaf(s[e], ap.cp, -rs.tau), ap, a0, a1, a2);
+            }
           }
         }
+        kglob += nkb;
         row_sum3(a0, a1, a2);
         alg1_update(rs, a0, a1, a2, ap);
       }
@@ -426,7 +452,9 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
   }
   ptx::tc_fence_before();
+  if (threadIdx.x == 0) ENTMAX_TRACE_EV(8006);
   ptx::cluster_sync();   // no CTA leaves while its peer may still multicast into it
+  if (threadIdx.x == 0) ENTMAX_TRACE_EV(8007);
   if (warp == kTauMathWarps + 1) ptx::tmem_dealloc<128 * kTauSBuf>(tmem);
 }
 

@@ -16,6 +16,7 @@ P.entmax_attn_fwd(q, k, v, 1.5, False, 3); torch.cuda.synchronize()
 L.entmax_trace_reset(int(sys.argv[2]) if len(sys.argv) > 2 else 30)
 P.entmax_attn_fwd(q, k, v, 1.5, False, 3); torch.cuda.synchronize()
 buf = np.zeros(8192, dtype=np.uint64); L.entmax_trace_read(buf.ctypes.data)
+t0 = 0
 print(f"CTAs {buf[8102]}  tier-1 rebuilds {buf[8100]}  tier-2 streaming {buf[8101]}")
 ev = buf[:8100]
 t0 = ev[ev > 0].min(); b = ev.astype(np.int64) - int(t0); b[ev == 0] = -1
@@ -32,3 +33,7 @@ print("math: wait for S", np.median(m_full[:n] - m_pre[:n]), " hold", np.median(
       " between tiles", np.median(m_pre[1:n] - m_rel[:n - 1]))
 print("latency MMA issue -> math sees S:", np.median(m_full[:n] - mma_se[:n]))
 print("CTA span (first..last event):", b[b >= 0].max(), "cycles;", b[b >= 0].max() / n, "per tile")
+t = lambda i: int(buf[i]) - int(t0) if buf[i] else -1
+print("phases (cycles from first event): start", t(8000), "math ready", t(8003), "stream done", t(8004),
+      "lists ready", t(8005), "pre-cluster-sync", t(8006), "end", t(8007))
+print("tail: iterations done", t(8008), "mask loop done", t(8009), "barrier", t(8010), "compacted", t(8011))
