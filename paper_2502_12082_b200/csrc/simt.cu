@@ -95,17 +95,27 @@ int simt_bwd_launch(int dtype, int d, int ecode, const void* q, const void* k, c
                          dk, dv, st);
 }
 
-int delta_launch(int dtype, const void* dO, const void* o2, const Geom& g, float* delta, cudaStream_t st) {
+template <typename T>
+static void delta_go(const T* dO, const float* o2, const Geom& g, float* delta, cudaStream_t st) {
   const long long rows = (long long)g.B * g.H * g.N;
-  const int threads = 256;
-  const long long blocks = (rows * 32 + threads - 1) / threads;
+  const int tpr = g.d / 8;
+  const unsigned blocks = (unsigned)((rows * tpr + 255) / 256);
+  switch (tpr) {
+    case 2: delta_kernel<T, 2><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
+    case 4: delta_kernel<T, 4><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
+    case 8: delta_kernel<T, 8><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
+    default: delta_kernel<T, 16><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
+  }
+}
+
+int delta_launch(int dtype, const void* dO, const void* o2, const Geom& g, float* delta, cudaStream_t st) {
+  if (g.d != 16 && g.d != 32 && g.d != 64 && g.d != 128) return fail(ENTMAX_ERR_UNSUPPORTED, "delta: d = %d not supported", g.d);
   {
     ProfScope ps("delta", st);
     if (dtype == ENTMAX_FP32)
-      delta_kernel<float><<<(unsigned)blocks, threads, 0, st>>>((const float*)dO, (const float*)o2, g, delta);
+      delta_go<float>(static_cast<const float*>(dO), static_cast<const float*>(o2), g, delta, st);
     else
-      delta_kernel<__nv_bfloat16><<<(unsigned)blocks, threads, 0, st>>>((const __nv_bfloat16*)dO,
-                                                                        (const float*)o2, g, delta);
+      delta_go<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(dO), static_cast<const float*>(o2), g, delta, st);
   }
   return cuda_status("delta");
 }

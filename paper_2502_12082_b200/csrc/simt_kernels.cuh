@@ -289,22 +289,47 @@ __global__ void __launch_bounds__(128) dq_kernel(const T* __restrict__ q, const 
 // Kernels shared by both implementations
 // ---------------------------------------------------------------------------------------
 
-// δ_i = dO_iᵀ O⁽²⁾_i: one warp per row, fp32 accumulation.
+// δ_i = dO_iᵀ O⁽²⁾_i, fp32 accumulation.  HBM-bound: TPR = d/8 threads per row, each
+// reading 8 consecutive elements of dO (one 16-byte vector for bf16) and of O⁽²⁾ (two float4), then a
+// TPR-lane shuffle reduction; 256 / TPR rows per 256-thread block.
 template <typename T>
-__global__ void delta_kernel(const T* __restrict__ dO, const float* __restrict__ o2, Geom g, float* __restrict__ delta) {
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long total = (long long)g.B * g.H * g.N;
-  if (warp >= total) return;
-  const int bh = (int)(warp / g.N);
-  const int r = (int)(warp - (long long)bh * g.N);
-  const long long off = g.head_off(bh) + (long long)r * g.sn;
-  const float* o2r = o2 + warp * g.d;   // fp32 contiguous [B,H,N,d]
-  float s = 0.f;
-  for (int c = lane; c < g.d; c += 32) s = fmaf(to_f<T>(dO[off + c]), o2r[c], s);
+__device__ __forceinline__ void load8(const T* p, float (&v)[8]);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 x = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-  for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-  if (lane == 0) delta[warp] = s;
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+template <typename T, int TPR>
+__global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, const float* __restrict__ o2, Geom g,
+                                                    float* __restrict__ delta) {
+  const long long row = ((long long)blockIdx.x * 256 + threadIdx.x) / TPR;
+  const int sub = threadIdx.x % TPR;
+  const long long total = (long long)g.B * g.H * g.N;
+  const bool ok = row < total;
+  float s = 0.f;
+  if (ok) {
+    const int bh = (int)(row / g.N);
+    const int r = (int)(row - (long long)bh * g.N);
+    float a[8], b[8];
+    load8<T>(dO + g.head_off(bh) + (long long)r * g.sn + sub * 8, a);
+    load8<float>(o2 + row * g.d + sub * 8, b);   // fp32 contiguous [B,H,N,d]
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s = fmaf(a[e], b[e], s);
+  }
+#pragma unroll
+  for (int m = TPR / 2; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  if (ok && sub == 0) delta[row] = s;
 }
 
 // 𝒦_j = {i | M_ij = 1} from the mask, increasing i; one thread per (head, j).
