@@ -261,12 +261,14 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 
     // Σ over the row's four column quarters in a fixed order (every thread of the row gets the
     // identical sums, so the four Alg. 1 updates agree bit for bit)
+    // (only the four warps that share the row's TMEM lane quadrant take part: barrier 2 + quadrant)
     auto row_sum3 = [&](float& a0, float& a1, float& a2) {
-      ptx::named_bar_sync(1, kTauMath);
+      const uint32_t qbar = 2u + (uint32_t)(warp & 3);
+      ptx::named_bar_sync(qbar, 128);
       xch[tid] = a0;
       xch[kTauMath + tid] = a1;
       xch[2 * kTauMath + tid] = a2;
-      ptx::named_bar_sync(1, kTauMath);
+      ptx::named_bar_sync(qbar, 128);
       a0 = (xch[r] + xch[128 + r]) + (xch[256 + r] + xch[384 + r]);
       a1 = (xch[kTauMath + r] + xch[kTauMath + 128 + r]) + (xch[kTauMath + 256 + r] + xch[kTauMath + 384 + r]);
       a2 = (xch[2 * kTauMath + r] + xch[2 * kTauMath + 128 + r]) +
@@ -387,9 +389,17 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       // and the row's four quarters combine in a fixed order (row_sum3), so τ is bitwise reproducible.
       if (tid == 0) ENTMAX_TRACE_EV(8005);
       const int n = list_len();
+      // the first kReg entries live in registers for all T iterations (−∞ pads contribute zeros)
+      constexpr int kReg = 12;
+      float lr[kReg];
+#pragma unroll
+      for (int c = 0; c < kReg; ++c) lr[c] = c < n ? ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u) : -INFINITY;
       for (int t = 0; t < n_iter; ++t) {
         float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-        for (int c = 0; c < n; ++c)
+#pragma unroll
+        for (int c = 0; c < kReg; ++c) accum_f<E>(fmaf(lr[c], ap.cp, -rs.tau), ap, a0, a1, a2);
+#pragma unroll 4
+        for (int c = kReg; c < n; ++c)
           accum_f<E>(fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau), ap, a0, a1, a2);
         row_sum3(a0, a1, a2);
         alg1_update(rs, a0, a1, a2, ap);
@@ -398,9 +408,14 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       if (valid) {
         if (qc == 0) tau_out[(long long)bh * g.N + row] = rs.tau;
         // exact block activity from the final τ (same fma test as the output kernel)
-        for (int c = 0; c < n; ++c)
+        const uint32_t af = ptx::smem_u32(aflag);
+#pragma unroll
+        for (int c = 0; c < kReg; ++c)
+          if (fmaf(lr[c], ap.cp, -rs.tau) > 0.f) ptx::st_shared_u8(af + ptx::ld_shared_u16(lj0 + (uint32_t)c * 256u), 1);
+#pragma unroll 4
+        for (int c = kReg; c < n; ++c)
           if (fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau) > 0.f)
-            aflag[ptx::ld_shared_u16(lj0 + (uint32_t)c * 256u)] = 1;
+            ptx::st_shared_u8(af + ptx::ld_shared_u16(lj0 + (uint32_t)c * 256u), 1);
       }
       if (tid == 0) ENTMAX_TRACE_EV(8009);
       ptx::named_bar_sync(1, kTauMath);

@@ -11,10 +11,12 @@ L = P._lib.lib()
 L.entmax_trace_reset.argtypes = [ctypes.c_int]; L.entmax_trace_read.argtypes = [ctypes.c_void_p]
 gen = sys.argv[1] if len(sys.argv) > 1 else "gaussian"
 rho = float(sys.argv[3]) if len(sys.argv) > 3 else 1 / 64
-q, k, v, do = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in synth.make_inputs(4, 12, 8192, 64, 7, synth.HeadSpec(gen, rho=rho))]
-P.entmax_attn_fwd(q, k, v, 1.5, False, 3); torch.cuda.synchronize()
+B, H, N, d = map(int, os.environ.get("SHAPE", "4 12 8192 64").split())
+alpha = float(os.environ.get("ALPHA", "1.5")); causal = os.environ.get("CAUSAL", "0") == "1"
+q, k, v, do = [torch.from_numpy(x).to(torch.bfloat16).cuda() for x in synth.make_inputs(B, H, N, d, 7, synth.HeadSpec(gen, rho=rho))]
+P.entmax_attn_fwd(q, k, v, alpha, causal, 3); torch.cuda.synchronize()
 L.entmax_trace_reset(int(sys.argv[2]) if len(sys.argv) > 2 else 30)
-P.entmax_attn_fwd(q, k, v, 1.5, False, 3); torch.cuda.synchronize()
+P.entmax_attn_fwd(q, k, v, alpha, causal, 3); torch.cuda.synchronize()
 buf = np.zeros(8192, dtype=np.uint64); L.entmax_trace_read(buf.ctypes.data)
 t0 = 0
 print(f"CTAs {buf[8102]}  tier-1 rebuilds {buf[8100]}  tier-2 streaming {buf[8101]}")
