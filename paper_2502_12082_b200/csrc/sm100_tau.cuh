@@ -161,13 +161,15 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     };
     for (int t = 0; t < nkb + W; ++t) load(t < nkb ? t : t - nkb);
     ptx::mbar_wait(&dec_bar, 0);
-    if (s_fallback) {
+    int fb = s_fallback;
+    if (fb == 1) {
       for (int j = 0; j < nkb; ++j) load(j);                 // tier 1
       ptx::mbar_wait(&dec_bar, 1);
-      if (s_fallback > 1)
-        for (int t = 0; t < n_iter; ++t)
-          for (int j = 0; j < nkb; ++j) load(j);             // tier 2
+      fb = s_fallback;
     }
+    if (fb == 2)
+      for (int t = 0; t < n_iter; ++t)
+        for (int j = 0; j < nkb; ++j) load(j);               // tier 2
   } else if (warp == kTauMathWarps + 1) {
     // ---------------------------------------------------------------- MMA issuer
     ptx::mbar_wait(&bar_q, 0);
@@ -187,12 +189,14 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     };
     for (int p = 0; p < nkb + W; ++p) mma();
     ptx::mbar_wait(&dec_bar, 0);
-    if (s_fallback) {
+    int fb = s_fallback;
+    if (fb == 1) {
       for (int p = 0; p < nkb; ++p) mma();
       ptx::mbar_wait(&dec_bar, 1);
-      if (s_fallback > 1)
-        for (int p = 0; p < n_iter * nkb; ++p) mma();
+      fb = s_fallback;
     }
+    if (fb == 2)
+      for (int p = 0; p < n_iter * nkb; ++p) mma();
   } else {
     // ---------------------------------------------------------------- math warps (512 threads)
     const int tid = threadIdx.x;
@@ -253,7 +257,10 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&s_peer_overflow[use]), peer), (uint32_t)flag);
         ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&x_bar), peer));
         ptx::mbar_wait_cluster(&x_bar, use);
-        s_fallback = (flag | s_peer_overflow[use]) ? 1 + use : 0;
+        // 0: lists complete; 1: rebuild them with the exact threshold (tier 1); 2: stream Alg. 3
+        // passes (tier 2) — taken directly when a list is more than twice over its capacity
+        const int any = flag | s_peer_overflow[use];
+        s_fallback = any == 0 ? 0 : (use == 1 || (any & 2)) ? 2 : 1;
       }
       ptx::named_bar_sync(1, kTauMath);
       return s_fallback != 0;
@@ -365,11 +372,19 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const float n_vis = g.causal ? (float)(row + 1) : (float)g.N;
     RowState rs = bracket_init(smax * ap.cp, n_vis, ap.alpha);
     thr = thr_of(smax);
-    if (list_len() > kCapQ) s_overflow = 1;
+    if (list_len() > kCapQ) {
+      // overflow: estimate the exact-threshold list length from the stored entries that pass the
+      // final threshold, extrapolated to every hit; if even that exceeds the capacity, a tier-1
+      // rebuild would overflow too, so go straight to tier 2
+      int above = 0;
+      for (int c = 0; c < kCapQ; ++c) above += ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u) > thr ? 1 : 0;
+      atomicOr(&s_overflow, above * list_len() > kCapQ * kCapQ ? 3 : 1);
+    }
     bool fallback = pair_any(0);
-    if (tid == 0 && fallback) ENTMAX_TRACE_COUNT(8100);
+    if (tid == 0 && s_fallback == 1) ENTMAX_TRACE_COUNT(8100);
+    if (tid == 0 && s_fallback == 2) ENTMAX_TRACE_COUNT(8103);
     if (tid == 0) ENTMAX_TRACE_COUNT(8102);
-    if (fallback) {
+    if (s_fallback == 1) {
       // tier 1: rebuild the lists with the exact threshold
       if (tid == 0) {
         ptx::mbar_arrive(&dec_bar);

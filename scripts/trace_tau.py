@@ -19,7 +19,7 @@ L.entmax_trace_reset(int(sys.argv[2]) if len(sys.argv) > 2 else 30)
 P.entmax_attn_fwd(q, k, v, alpha, causal, 3); torch.cuda.synchronize()
 buf = np.zeros(8192, dtype=np.uint64); L.entmax_trace_read(buf.ctypes.data)
 t0 = 0
-print(f"CTAs {buf[8102]}  tier-1 rebuilds {buf[8100]}  tier-2 streaming {buf[8101]}")
+print(f"CTAs {buf[8102]}  tier-1 rebuilds {buf[8100]}  tier-2 streaming after tier 1 {buf[8101]}, directly {buf[8103]}")
 ev = buf[:8100]
 t0 = ev[ev > 0].min(); b = ev.astype(np.int64) - int(t0); b[ev == 0] = -1
 n = int((b[0:1024:4] >= 0).sum())
