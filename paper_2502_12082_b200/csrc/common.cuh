@@ -133,10 +133,35 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
-// P and U for a pair of x values (same semantics as p_and_u), FMA-pipe friendly for E = 1, 2.
+// Generic α: U = x^{e−1} = 2^{(e−1)·log2 x} and P = U·x for a pair of x with two
+// MUFU ops per element (lg2.approx.ftz, ex2.approx.ftz) and three other instructions, instead of an
+// accurate exp2f per power (the tensor-core kernels are issue-bound there, so the instruction count is
+// what matters: an FMA-pipe polynomial exp2 measured slower).  Relative error of U, P ≈ 2^-21·max(1,
+// (e−1)·|log2 x|) — far below the bf16 rounding (2^-9) they get as MMA operands.  x <= 0 (or −∞ for
+// masked keys) gives exactly 0; ex2.approx.ftz flushes an underflowing U to 0.
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void pu_generic2(float2 x, float em1, float2& p, float2& u) {
+  const float2 y = fmul2(make_float2(lg2_approx(x.x), lg2_approx(x.y)), make_float2(em1, em1));
+  u = make_float2(x.x > 0.f ? ex2_approx(y.x) : 0.f, x.y > 0.f ? ex2_approx(y.y) : 0.f);
+  p = fmul2(u, make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f)));
+}
+
+// P and U for a pair of x values (same semantics as p_and_u), FMA-pipe friendly for E = 1, 2 and the
+// generic α path (E = 0).
 template <int E>
 __device__ __forceinline__ void p_and_u2(float2 x, const AlphaParams& ap, float2& p, float2& u) {
-  if (E == 2) {
+  if (E == 0) {
+    pu_generic2(x, ap.em1, p, u);
+  } else if (E == 2) {
     u = make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f));
     p = fmul2(u, u);
   } else if (E == 1) {
