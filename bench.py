@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--sweep", action="store_true", help="add the planted block-sparsity sweep")
+    ap.add_argument("--sweep", action="store_true", default=True,
+                    help="add the planted block-sparsity sweep (default on; --no-sweep to skip)")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--suite", action="store_true", help="add configs 3-5 (seq-len / alpha / long-context lines)")
     ap.add_argument("--no-rowwise", action="store_true", help="skip the standalone row-wise solver line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -146,15 +148,16 @@ def load_peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sustained=1400.0, src="fallback (B200_PROFILING.md)")
 
 
-def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+def ncu_traffic(kernel, key="dram_bytes_per_launch"):
+    """DRAM bytes per launch (or another field, e.g. tensor_pipe_pct) of `kernel` from the committed
+    ncu --set full summary (profiles/ncu_traffic.json), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as fh:
         d = json.load(fh)
     ent = d.get(kernel)
-    return None if ent is None else ent.get("dram_bytes_per_launch")
+    return None if ent is None else ent.get(key)
 
 
 # ------------------------------------------------------------------------------ oracle legs
@@ -376,7 +379,9 @@ def main():
     dom = max(prof, key=lambda n: prof[n][1])
     vis_all = B * H * total_visible_pairs(N, causal)
     mma_flops = {
-        "tau_sm100": (1 + n_iter) * 2.0 * d * vis_all,          # 1 max pass + T passes of S = QKᵀ
+        # one streaming pass of S = QKᵀ + the nkb/4 warm-up tiles it re-streams (the paper's Alg. 3 would
+        # issue 1 + T passes; fallback tiers, taken by a few % of CTAs, are not counted)
+        "tau_sm100": 1.25 * 2.0 * d * vis_all,
         "out_sm100": 6.0 * d * pairs,                             # S, P·V, U·V on candidate blocks
         "dkdv_sm100": 8.0 * d * pairs,                            # Sᵀ, dPᵀ, Pᵀ·dO, dSᵀ·Q
         "dq_sm100": 6.0 * d * pairs,                              # S, dP, dS·K
@@ -389,7 +394,11 @@ def main():
                 "peak_src": peaks["src"] + " bf16_tflops_sustained (kernel timed inside the step)",
                 "algorithmic": "MMA flops issued per launch (see DESIGN.md §Roofline)"}
     kernels = {n: {"launches_per_step": c / args.steps, "ms_per_launch": kern_ms[n],
-                   "share": tot / sum(t for _, t in prof.values())} for n, (c, tot) in prof.items()}
+                   "share": tot / sum(t for _, t in prof.values()),
+                   **({"achieved_tflops": mma_flops[n] / (kern_ms[n] * 1e-3) / 1e12,
+                       "frac_of_sustained_bf16": mma_flops[n] / (kern_ms[n] * 1e-3) / 1e12 / peaks["bf16_sustained"],
+                       "ncu_tensor_pipe_pct": ncu_traffic(n, "tensor_pipe_pct")} if n in mma_flops else {})}
+               for n, (c, tot) in prof.items()}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

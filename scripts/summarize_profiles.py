@@ -68,7 +68,9 @@ for raw in sorted(glob.glob(os.path.join(src, f"{tag}_full_*_raw.csv"))):
     ent["dram_bytes_per_launch"] = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
     summary[case] = ent
     if case in NAMES:
+        tp = "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"
         traffic[NAMES[case]] = {"dram_bytes_per_launch": ent["dram_bytes_per_launch"],
+                                "tensor_pipe_pct": float(r[idx[tp]]) if tp in idx else None,
                                 "ncu_kernel": ent["kernel"].split("(")[0], "round": tag,
                                 "input": "config 2 Gaussian (scripts/run_fwd.py gaussian 1.0 bwd)"}
     # stall breakdown from the source page
