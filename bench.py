@@ -431,6 +431,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()          # rank 0's extra lines (sweep, row-wise, CPU baseline) finish first
         dist.destroy_process_group()
 
 
