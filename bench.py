@@ -544,11 +544,26 @@ def run_suite(P, synth, torch, dev, args):
             P.entmax_attn_fwd(q, k, v, alpha, causal, 3, out=fw)
             P.entmax_attn_bwd(q, k, v, do, fw, alpha, causal, grads=g)
         fb_ms = _time(torch, fb, it)
+        # the same step captured once in a CUDA graph and replayed (no per-launch CPU overhead)
+        gms = None
+        try:
+            s_ = torch.cuda.Stream(dev)
+            s_.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(s_):
+                fb()
+            torch.cuda.current_stream(dev).wait_stream(s_)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                fb()
+            gms = _time(torch, graph.replay, it)
+            del graph
+        except Exception:
+            pass
         pairs = visible_pairs_in_active_blocks(fw.mask, N, causal)
         sd = sdpa_ms(torch, q, k, v, do, causal, iters=it)
         out.append({"config": name, "B": B, "H": H, "N": N, "d": d, "alpha": alpha, "causal": causal,
                     "block_density": pairs / (B * H * total_visible_pairs(N, causal)),
-                    "fwd_ms": f_ms, "fwd_bwd_ms": fb_ms,
+                    "fwd_ms": f_ms, "fwd_bwd_ms": fb_ms, "fwd_bwd_ms_cuda_graph": gms,
                     "eff_tflops_fwd": 4.0 * d * pairs / (f_ms * 1e-3) / 1e12,
                     "eff_tflops_fwd_bwd": 14.0 * d * pairs / (fb_ms * 1e-3) / 1e12,
                     "sdpa_fwd_bwd_ms": sd})

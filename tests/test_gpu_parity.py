@@ -124,3 +124,49 @@ def test_parity_transient_overflow_rebuild(N, causal):
     fw, grads = run_gpu(dev, 1.5, causal, 3)
     for bh in range(2):
         check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
+
+
+@pytest.mark.parametrize("alpha,causal,d", [(1.1, False, 64), (1.33, True, 64), (1.9, False, 64), (1.6, True, 128)])
+def test_parity_generic_alpha(alpha, causal, d):
+    """Non-integer 1/(α−1): P, U via lg2/ex2 in the tcgen05 kernels, the τ sums
+    via the generic accumulation.  α = 1.1 gives e = 10 (steep powers), α = 1.9 e ≈ 1.11."""
+    _require_gpu()
+    dev, ref = make_case(1, 2, 640, d, torch.bfloat16, seed=int(alpha * 100) + d)
+    fw, grads = run_gpu(dev, alpha, causal, 4)
+    for bh in range(2):
+        check_head(fw, ref, bh, alpha, causal, 4, torch.bfloat16, grads=grads)
+
+
+def test_cuda_graph_capture_replays_bitwise():
+    """The C ABI is stream-ordered with no host synchronisation or allocation inside, so a whole
+    fwd+bwd step can be captured in a CUDA graph (launch-bound small configs) and replayed."""
+    _require_gpu()
+    import paper_2502_12082_b200 as P
+    dev, _ = make_case(2, 3, 1024, 64, torch.bfloat16, seed=21)
+    q, k, v, do = dev
+    fw = P.entmax_attn_fwd(q, k, v, 1.5, True, 3)
+    ws_f = torch.empty(P.workspace_bytes(q, True)[0], dtype=torch.uint8, device=q.device)
+    ws_b = torch.empty(P.workspace_bytes(q, True)[1], dtype=torch.uint8, device=q.device)
+    grads = tuple(torch.empty_like(t) for t in (q, k, v))
+
+    def step():
+        P.entmax_attn_fwd(q, k, v, 1.5, True, 3, out=fw, workspace=ws_f)
+        P.entmax_attn_bwd(q, k, v, do, fw, 1.5, True, grads=grads, workspace=ws_b)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    ref_o, ref_g = fw.o.clone(), [g.clone() for g in grads]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for t in (fw.o, *grads):
+        t.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(fw.o, ref_o)
+    for a, b in zip(grads, ref_g):
+        assert torch.equal(a, b)
