@@ -20,6 +20,11 @@ P.entmax_attn_fwd(q, k, v, alpha, causal, 3); torch.cuda.synchronize()
 buf = np.zeros(8192, dtype=np.uint64); L.entmax_trace_read(buf.ctypes.data)
 t0 = 0
 print(f"CTAs {buf[8102]}  tier-1 rebuilds {buf[8100]}  tier-2 streaming after tier 1 {buf[8101]}, directly {buf[8103]}")
+t0 = int(buf[:8100][buf[:8100] > 0].min())
+t = lambda i: int(buf[i]) - int(t0) if buf[i] else -1
+print("phases (cycles from first event): start", t(8000), "math ready", t(8003), "stream done", t(8004),
+      "lists ready", t(8005), "pre-cluster-sync", t(8006), "end", t(8007))
+print("tail: iterations done", t(8008), "mask loop done", t(8009), "barrier", t(8010), "compacted", t(8011))
 ev = buf[:8100]
 t0 = ev[ev > 0].min(); b = ev.astype(np.int64) - int(t0); b[ev == 0] = -1
 n = int((b[0:1024:4] >= 0).sum())
@@ -35,7 +40,3 @@ print("math: wait for S", np.median(m_full[:n] - m_pre[:n]), " hold", np.median(
       " between tiles", np.median(m_pre[1:n] - m_rel[:n - 1]))
 print("latency MMA issue -> math sees S:", np.median(m_full[:n] - mma_se[:n]))
 print("CTA span (first..last event):", b[b >= 0].max(), "cycles;", b[b >= 0].max() / n, "per tile")
-t = lambda i: int(buf[i]) - int(t0) if buf[i] else -1
-print("phases (cycles from first event): start", t(8000), "math ready", t(8003), "stream done", t(8004),
-      "lists ready", t(8005), "pre-cluster-sync", t(8006), "end", t(8007))
-print("tail: iterations done", t(8008), "mask loop done", t(8009), "barrier", t(8010), "compacted", t(8011))
