@@ -465,6 +465,14 @@ def run_sweep(P, synth, torch, dev, cfg, args):
             e1.record()
             torch.cuda.synchronize()
             res[name] = e0.elapsed_time(e1) / max(5, args.steps // 2)
+        # the paper's unmasked variant (NEXT-2: every visible block, no tables) on the same inputs
+        fwu = P.entmax_attn_fwd(q, k, v, cfg["alpha"], cfg["causal"], cfg["n_iter"], masked=False)
+
+        def fbu():
+            P.entmax_attn_fwd(q, k, v, cfg["alpha"], cfg["causal"], cfg["n_iter"], out=fwu, masked=False)
+            P.entmax_attn_bwd(q, k, v, do, fwu, cfg["alpha"], cfg["causal"], grads=g)
+
+        res["fwd_bwd_unmasked"] = _time(torch, fbu, max(5, args.steps // 2))
         fb()
         torch.cuda.synchronize()
         pairs = visible_pairs_in_active_blocks(fw.mask, N, cfg["causal"])
@@ -472,9 +480,10 @@ def run_sweep(P, synth, torch, dev, cfg, args):
         # dense softmax reference on the same box (cuDNN / flash SDPA, FA-convention flops)
         sd = sdpa_ms(torch, q, k, v, do, cfg["causal"]) if rho == 1.0 else None
         out.append({"rho_target": rho, "block_density": dens, "fwd_ms": res["fwd"], "fwd_bwd_ms": res["fwd_bwd"],
+                    "fwd_bwd_ms_unmasked": res["fwd_bwd_unmasked"],
                     "eff_tflops_fwd_bwd": 14.0 * d * pairs / (res["fwd_bwd"] * 1e-3) / 1e12,
                     **({"sdpa_fwd_bwd_ms": sd} if sd else {})})
-        del q, k, v, do, fw, g
+        del q, k, v, do, fw, fwu, g
     return out
 
 

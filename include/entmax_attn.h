@@ -89,6 +89,11 @@ size_t entmax_attn_bwd_workspace_bytes(const entmax_shape_t* shp, int dtype, int
  *   tau           out: [B,H,N] fp32 (after the T-th update, reading c4).
  *   mask          out: [B,H,T_r,T_c] uint8 (see conventions).
  *   row_cnt/row_idx out: 𝒬 tables (see conventions).
+ *                 mask, row_cnt and row_idx may ALL be NULL: the unmasked mode (the paper's variant
+ *                 without block masking) visits every
+ *                 visible K/V block and writes neither M nor the tables (O(N) extra memory); the
+ *                 backward must then be called with NULL tables too.  Some but not all NULL →
+ *                 ENTMAX_ERR_INVALID_ARG.
  *   workspace     in : device scratch of >= entmax_attn_fwd_workspace_bytes bytes.
  *   stream        in : cudaStream_t.
  */
@@ -101,7 +106,8 @@ int entmax_attn_fwd(const void* q, const void* k, const void* v, const entmax_sh
  * Backward pass (App. A.2, Algs. 4-5 with the lookup tables).
  *   q, k, v, d_o  in : [B,H,N,d] dtype.  o2 in: [B,H,N,d] fp32 contiguous from the forward
  *                      (O itself is not needed).
- *   tau, mask, row_cnt, row_idx in : exactly as written by entmax_attn_fwd for these inputs.
+ *   tau, mask, row_cnt, row_idx in : exactly as written by entmax_attn_fwd for these inputs
+ *                      (mask, row_cnt, row_idx all NULL: unmasked mode, every visible block).
  *   alpha, causal, scale      in : the forward's values.
  *   dq, dk, dv    out: [B,H,N,d] dtype.  dQ = c·dS K, dK = c·dSᵀ Q, dV = Pᵀ dO.
  *   workspace     in : >= entmax_attn_bwd_workspace_bytes bytes (holds δ and the 𝒦 tables).

@@ -91,8 +91,10 @@ class FwdResult:
 
 
 def entmax_attn_fwd(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, training=True,
-                    out: FwdResult | None = None, workspace: torch.Tensor | None = None) -> FwdResult:
-    """Forward pass through the C ABI (see include/entmax_attn.h)."""
+                    out: FwdResult | None = None, workspace: torch.Tensor | None = None,
+                    masked: bool = True) -> FwdResult:
+    """Forward pass through the C ABI (see include/entmax_attn.h).  masked=False selects the
+    unmasked mode (no block skipping; mask/row_cnt/row_idx are None)."""
     _check_inputs(q, k, v)
     L = _lib.lib()
     s = _shape(q)
@@ -105,9 +107,9 @@ def entmax_attn_fwd(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, trai
             o=torch.empty_like(q),
             o2=torch.empty(q.shape, dtype=torch.float32, device=dev) if training else None,
             tau=torch.empty((B, H, N), dtype=torch.float32, device=dev),
-            mask=torch.empty((B, H, Tr, Tc), dtype=torch.uint8, device=dev),
-            row_cnt=torch.empty((B, H, Tr), dtype=torch.int32, device=dev),
-            row_idx=torch.empty((B, H, Tr, Tc), dtype=torch.int32, device=dev))
+            mask=torch.empty((B, H, Tr, Tc), dtype=torch.uint8, device=dev) if masked else None,
+            row_cnt=torch.empty((B, H, Tr), dtype=torch.int32, device=dev) if masked else None,
+            row_idx=torch.empty((B, H, Tr, Tc), dtype=torch.int32, device=dev) if masked else None)
     ws_bytes = L.entmax_attn_fwd_workspace_bytes(ctypes.byref(s), _DT[q.dtype], int(causal))
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
@@ -144,9 +146,9 @@ def entmax_attn_bwd(q, k, v, d_o, fwd: FwdResult, alpha=1.5, causal=False, scale
 
 class _EntmaxAttention(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, alpha, causal, n_iter, scale):
+    def forward(ctx, q, k, v, alpha, causal, n_iter, scale, masked):
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
-        fw = entmax_attn_fwd(q, k, v, alpha, causal, n_iter, scale, training=True)
+        fw = entmax_attn_fwd(q, k, v, alpha, causal, n_iter, scale, training=True, masked=masked)
         ctx.save_for_backward(q, k, v, fw.o2, fw.tau, fw.mask, fw.row_cnt, fw.row_idx)
         ctx.cfg = (alpha, causal, scale)
         return fw.o
@@ -157,12 +159,13 @@ class _EntmaxAttention(torch.autograd.Function):
         alpha, causal, scale = ctx.cfg
         fw = FwdResult(None, o2, tau, mask, row_cnt, row_idx)
         dq, dk, dv = entmax_attn_bwd(q, k, v, d_o.contiguous(), fw, alpha, causal, scale)
-        return dq, dk, dv, None, None, None, None
+        return dq, dk, dv, None, None, None, None, None
 
 
-def entmax_attention(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None):
-    """α-entmax attention O = entmax_α(QKᵀ/√d) V with AdaSplash block skipping (autograd op)."""
-    return _EntmaxAttention.apply(q, k, v, alpha, causal, n_iter, scale)
+def entmax_attention(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, masked=True):
+    """α-entmax attention O = entmax_α(QKᵀ/√d) V with AdaSplash block skipping (autograd op);
+    masked=False: the paper's unmasked variant (every visible block, no mask/tables stored)."""
+    return _EntmaxAttention.apply(q, k, v, alpha, causal, n_iter, scale, masked)
 
 
 def profile_enable(on: bool = True):

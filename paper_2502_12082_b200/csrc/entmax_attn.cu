@@ -215,8 +215,10 @@ int entmax_attn_fwd(const void* q, const void* k, const void* v, const entmax_sh
   if (int rc = check_shape(shp, dtype)) return rc;
   if (int rc = check_alpha(alpha)) return rc;
   if (n_iter < 1) return fail(ENTMAX_ERR_INVALID_ARG, "n_iter must be >= 1 (got %d)", n_iter);
-  if (!q || !k || !v || !o || !tau || !mask || !row_cnt || !row_idx)
-    return fail(ENTMAX_ERR_INVALID_ARG, "NULL tensor pointer");
+  if (!q || !k || !v || !o || !tau) return fail(ENTMAX_ERR_INVALID_ARG, "NULL tensor pointer");
+  // mask, row_cnt, row_idx: all set (block-sparse mode) or all NULL (unmasked mode, NEXT-2)
+  if ((mask == nullptr) != (row_cnt == nullptr) || (mask == nullptr) != (row_idx == nullptr))
+    return fail(ENTMAX_ERR_INVALID_ARG, "mask, row_cnt and row_idx must be all set or all NULL (unmasked mode)");
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || (o2 && !aligned16(o2)))
     return fail(ENTMAX_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
   const FwdWs wl = fwd_ws_layout(*shp);
@@ -244,8 +246,10 @@ int entmax_attn_bwd(const void* q, const void* k, const void* v, const void* o2,
   g_last_error.clear();
   if (int rc = check_shape(shp, dtype)) return rc;
   if (int rc = check_alpha(alpha)) return rc;
-  if (!q || !k || !v || !o2 || !d_o || !tau || !mask || !row_cnt || !row_idx || !dq || !dk || !dv)
-    return fail(ENTMAX_ERR_INVALID_ARG, "NULL tensor pointer");
+  if (!q || !k || !v || !o2 || !d_o || !tau || !dq || !dk || !dv) return fail(ENTMAX_ERR_INVALID_ARG, "NULL tensor pointer");
+  if ((mask == nullptr) != (row_cnt == nullptr) || (mask == nullptr) != (row_idx == nullptr))
+    return fail(ENTMAX_ERR_INVALID_ARG, "mask, row_cnt and row_idx must be all set or all NULL (unmasked mode)");
+  const bool unmasked = mask == nullptr;
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o2) || !aligned16(d_o) || !aligned16(dq) ||
       !aligned16(dk) || !aligned16(dv))
     return fail(ENTMAX_ERR_INVALID_ARG, "tensor pointers must be 16-byte aligned");
@@ -261,12 +265,14 @@ int entmax_attn_bwd(const void* q, const void* k, const void* v, const void* o2,
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)workspace;
   float* delta = (float*)(ws + wl.delta);
-  int32_t* col_cnt = (int32_t*)(ws + wl.col_cnt);
-  int32_t* col_idx = (int32_t*)(ws + wl.col_idx);
+  int32_t* col_cnt = unmasked ? nullptr : (int32_t*)(ws + wl.col_cnt);
+  int32_t* col_idx = unmasked ? nullptr : (int32_t*)(ws + wl.col_idx);
 
-  // δ and the 𝒦 tables — shared by both implementations
+  // δ and the 𝒦 tables — shared by both implementations; the unmasked
+  // mode visits every visible block and needs no tables
   if (int rc = delta_launch(dtype, d_o, o2, g, delta, st)) return rc;
-  if (int rc = col_lists_launch(mask, g, col_cnt, col_idx, st)) return rc;
+  if (!unmasked)
+    if (int rc = col_lists_launch(mask, g, col_cnt, col_idx, st)) return rc;
 
   if (impl == 1) {
     return sm100::bwd(q, k, v, d_o, g, ap, ecode, tau, delta, row_cnt, row_idx, col_cnt, col_idx, dq, dk, dv, st);

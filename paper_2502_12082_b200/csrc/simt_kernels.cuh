@@ -141,13 +141,15 @@ __global__ void __launch_bounds__(128) out_kernel(const T* __restrict__ q, const
       }
     }
     const int any = __syncthreads_or(act ? 1 : 0);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && mask) {   // (unmasked mode: no mask / table output)
       mrow[jb] = any ? 1 : 0;
       if (any) lrow[cnt++] = jb;
     }
   }
-  for (int jb = nkb + threadIdx.x; jb < g.Tc; jb += blockDim.x) mrow[jb] = 0;
-  if (threadIdx.x == 0) row_cnt[(long long)bh * g.Tr + i] = cnt;
+  if (mask) {
+    for (int jb = nkb + threadIdx.x; jb < g.Tc; jb += blockDim.x) mrow[jb] = 0;
+    if (threadIdx.x == 0) row_cnt[(long long)bh * g.Tr + i] = cnt;
+  }
   if (valid) {
     T* orow = o + hoff + (long long)r * g.sn;
 #pragma unroll
@@ -186,10 +188,12 @@ __global__ void __launch_bounds__(128) dkdv_kernel(const T* __restrict__ q, cons
     dka[c] = 0.f;
     dva[c] = 0.f;
   }
-  const int cnt = col_cnt[(long long)bh * g.Tc + jb];
-  const int32_t* lst = col_idx + ((long long)bh * g.Tc + jb) * g.Tr;
+  // unmasked mode (col_idx == nullptr): every query block that sees key block jb
+  const int i0 = g.causal ? (jb * kBc) / kBr : 0;
+  const int cnt = col_idx ? col_cnt[(long long)bh * g.Tc + jb] : g.Tr - i0;
+  const int32_t* lst = col_idx ? col_idx + ((long long)bh * g.Tc + jb) * g.Tr : nullptr;
   for (int t = 0; t < cnt; ++t) {
-    const int ib = lst[t];
+    const int ib = lst ? lst[t] : i0 + t;
     for (int rt = ib * kBr; rt < min(g.N, (ib + 1) * kBr); rt += KT) {
       __syncthreads();
       stage_rows<T, D>(qs, q + hoff, g.sn, rt, g.N);
@@ -252,10 +256,11 @@ __global__ void __launch_bounds__(128) dq_kernel(const T* __restrict__ q, const 
   }
   const float tr = valid ? tau[(long long)bh * g.N + row] : 0.f;
   const float dl = valid ? delta[(long long)bh * g.N + row] : 0.f;
-  const int cnt = row_cnt[(long long)bh * g.Tr + ib];
-  const int32_t* lst = row_idx + ((long long)bh * g.Tr + ib) * g.Tc;
+  // unmasked mode (row_idx == nullptr): every visible key block
+  const int cnt = row_idx ? row_cnt[(long long)bh * g.Tr + ib] : g.visible_kblocks(ib);
+  const int32_t* lst = row_idx ? row_idx + ((long long)bh * g.Tr + ib) * g.Tc : nullptr;
   for (int t = 0; t < cnt; ++t) {
-    const int jb = lst[t];
+    const int jb = lst ? lst[t] : t;
     for (int kt = jb * kBc; kt < min(g.N, (jb + 1) * kBc); kt += KT) {
       __syncthreads();
       stage_rows<T, D>(ks, k + hoff, g.sn, kt, g.N);

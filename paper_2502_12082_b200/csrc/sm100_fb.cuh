@@ -105,8 +105,9 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long li = (long long)bh * g.Tr + i;
-  const int ncand = cand_cnt[li];
-  const int32_t* list = cand_idx + li * g.Tc;
+  const bool dense = mask == nullptr;   // unmasked mode: every visible block, no mask / table output
+  const int ncand = dense ? g.visible_kblocks(i) : cand_cnt[li];
+  const BlockList list{dense ? nullptr : cand_idx + li * g.Tc, 0};
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
@@ -243,12 +244,14 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         }
       }
     }
-    ptx::named_bar_sync(1, kFbMath);
-    uint8_t* mrow = mask + li * g.Tc;
-    for (int j = tid; j < g.Tc; j += kFbMath) mrow[j] = aflag[j];
-    if (warp == 0) {
-      const int cnt = compact_flags(aflag, g.Tc, row_idx + li * g.Tc);
-      if (lane == 0) row_cnt[li] = cnt;
+    if (!dense) {
+      ptx::named_bar_sync(1, kFbMath);
+      uint8_t* mrow = mask + li * g.Tc;
+      for (int j = tid; j < g.Tc; j += kFbMath) mrow[j] = aflag[j];
+      if (warp == 0) {
+        const int cnt = compact_flags(aflag, g.Tc, row_idx + li * g.Tc);
+        if (lane == 0) row_cnt[li] = cnt;
+      }
     }
   }
   ptx::tc_fence_before();
@@ -282,8 +285,9 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5;
   const long long li = (long long)bh * g.Tr + i;
-  const int cnt = row_cnt[li];
-  const int32_t* list = row_idx + li * g.Tc;
+  const bool dense = row_idx == nullptr;   // unmasked mode: every visible key block
+  const int cnt = dense ? g.visible_kblocks(i) : row_cnt[li];
+  const BlockList list{dense ? nullptr : row_idx + li * g.Tc, 0};
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
@@ -433,8 +437,10 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long lj = (long long)bh * g.Tc + j;
-  const int cnt = col_cnt[lj];
-  const int32_t* list = col_idx + lj * g.Tr;
+  const bool dense = col_idx == nullptr;   // unmasked mode: every query block that sees key block j
+  const int i0 = g.causal ? (j * kBc) / kBr : 0;
+  const int cnt = dense ? g.Tr - i0 : col_cnt[lj];
+  const BlockList list{dense ? nullptr : col_idx + lj * g.Tr, i0};
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_kv, 1);

@@ -100,6 +100,14 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
 }
 
 // compact per-block flags flags[0..n) into an increasing index list (one math warp)
+// A block list: the compacted table entries, or — in the unmasked mode (table == nullptr, SURVEY §8f
+// NEXT-2, the paper's variant without block masking P:L398, L1073) — every visible block base, base+1, …
+struct BlockList {
+  const int32_t* idx;
+  int base;
+  __device__ __forceinline__ int operator[](int k) const { return idx ? __ldg(idx + k) : base + k; }
+};
+
 __device__ __forceinline__ int compact_flags(const uint8_t* flags, int n, int32_t* out) {
   const int lane = threadIdx.x & 31;
   int cnt = 0;

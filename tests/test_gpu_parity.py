@@ -170,3 +170,46 @@ def test_cuda_graph_capture_replays_bitwise():
     assert torch.equal(fw.o, ref_o)
     for a, b in zip(grads, ref_g):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype,d", [(torch.bfloat16, 64), (torch.bfloat16, 128), (torch.float32, 64)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_unmasked_mode_matches_masked_bitwise(dtype, d, causal):
+    """Unmasked mode (every visible block, no mask/tables): the skipped blocks of
+    the masked mode hold P = U = dS = 0 exactly, so both modes give the same bits; and the unmasked
+    mode matches the oracle on its own."""
+    _require_gpu()
+    import paper_2502_12082_b200 as P
+    spec = synth.HeadSpec("planted", rho=0.25)
+    dev, ref = make_case(1, 2, 1024, d, dtype, seed=31 + d, spec=spec)
+    q, k, v, do = dev
+    fm = P.entmax_attn_fwd(q, k, v, 1.5, causal, 3)
+    gm = P.entmax_attn_bwd(q, k, v, do, fm, 1.5, causal)
+    fu = P.entmax_attn_fwd(q, k, v, 1.5, causal, 3, masked=False)
+    gu = P.entmax_attn_bwd(q, k, v, do, fu, 1.5, causal)
+    torch.cuda.synchronize()
+    assert fu.mask is None and fu.row_idx is None
+    if not causal:
+        assert fm.mask.float().mean().item() < 0.5          # the masked run really skipped blocks
+    assert torch.equal(fu.tau, fm.tau) and torch.equal(fu.o, fm.o) and torch.equal(fu.o2, fm.o2)
+    for a, b in zip(gu, gm):
+        assert torch.equal(a, b)
+    o = P.entmax_attention(q.clone().requires_grad_(), k, v, 1.5, causal, 3, masked=False)
+    assert torch.equal(o.detach(), fu.o)
+    check_head(fm, ref, 0, 1.5, causal, 3, dtype, grads=gu)   # (the oracle's mask vs the masked run)
+
+
+def test_unmasked_mode_rejects_partial_null_tables():
+    _require_gpu()
+    import ctypes
+    import paper_2502_12082_b200 as P
+    from paper_2502_12082_b200 import _lib
+    dev, _ = make_case(1, 1, 256, 64, torch.bfloat16, seed=1)
+    q = dev[0]
+    fw = P.entmax_attn_fwd(q, q, q, 1.5, False, 3)
+    s = P._shape(q)
+    ws = torch.empty(P.workspace_bytes(q, False)[0], dtype=torch.uint8, device=q.device)
+    rc = _lib.lib().entmax_attn_fwd(P._ptr(q), P._ptr(q), P._ptr(q), ctypes.byref(s), 0, 1.5, 0, 3, 0.0,
+                                    P._ptr(fw.o), P._ptr(fw.o2), P._ptr(fw.tau), P._ptr(fw.mask), None, None,
+                                    P._ptr(ws), ws.numel(), None)
+    assert rc == 1
