@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
     ap.add_argument("--suite", action="store_true", help="add configs 3-5 (seq-len / alpha / long-context lines)")
     ap.add_argument("--no-rowwise", action="store_true", help="skip the standalone row-wise solver line")
+    ap.add_argument("--gpt2", action="store_true", help="add the GPT-2-124M training-step line (NEXT-4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--N", type=int, default=CFG["N"])
     ap.add_argument("--d", type=int, default=CFG["d"])
@@ -423,6 +424,10 @@ def main():
         line["suite"] = run_suite(P, synth, torch, dev, args)
     if not args.no_rowwise and rank == 0:
         line["next1_rowwise"] = run_rowwise(P, synth, torch, dev, peaks)
+    if args.gpt2 and rank == 0:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import gpt2_step
+        line["next4_gpt2"] = gpt2_step.run()
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, fl, desc = oracle_sample(dict(cfg), seed=0, rows=4096)
