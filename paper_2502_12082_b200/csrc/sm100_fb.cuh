@@ -139,9 +139,14 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     for (int k = 0; k < ncand; ++k) {
       const int j = list[k], st = k % NST;
       ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+#ifdef ENTMAX_FB_HALFTMA   // diagnostics: half the streamed bytes (results invalid)
+      ptx::mbar_arrive_expect_tx_elect(&kv_full[st], C::TILE);
+      tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], j * kBc, h, b);
+#else
       ptx::mbar_arrive_expect_tx_elect(&kv_full[st], 2 * C::TILE);
       tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], j * kBc, h, b);
       tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], j * kBc, h, b);
+#endif
     }
   } else if (warp == 9) {
     ptx::mbar_wait(&bar_q, 0);
@@ -318,9 +323,14 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     for (int k = 0; k < cnt; ++k) {
       const int jb = list[k], st = k % NST;
       ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+#ifdef ENTMAX_FB_HALFTMA
+      ptx::mbar_arrive_expect_tx_elect(&kv_full[st], C::TILE);
+      tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], jb * kBc, h, b);
+#else
       ptx::mbar_arrive_expect_tx_elect(&kv_full[st], 2 * C::TILE);
       tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], jb * kBc, h, b);
       tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], jb * kBc, h, b);
+#endif
     }
   } else if (warp == 9) {
     ptx::mbar_wait(&bar_q, 0);
@@ -484,9 +494,14 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
         dl_s[lane * 4 + e] = rr < g.N ? delta[(long long)bh * g.N + rr] : 0.f;
       }
       __syncwarp();
+#ifdef ENTMAX_FB_HALFTMA
+      ptx::mbar_arrive_expect_tx_elect(&qd_full[st], C::TILE);
+      tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
+#else
       ptx::mbar_arrive_expect_tx_elect(&qd_full[st], 2 * C::TILE);
       tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
       tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
+#endif
       __syncwarp();
     }
   } else if (warp == 9) {
