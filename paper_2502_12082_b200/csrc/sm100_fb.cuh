@@ -526,7 +526,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
       mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
       ptx::mma_commit_elect(&qd_empty[st]);
-      ptx::mma_commit_elect(&p_empty);
+      if (!ALIAS) ptx::mma_commit_elect(&p_empty);   // (aliased Pᵀ/dSᵀ: the next Sᵀ MMA orders it)
       if (ALIAS && k + 1 < cnt) issue_sdp(k + 1);
     }
     ptx::mma_commit_elect(&acc_full);

@@ -14,8 +14,8 @@
 // The first W blocks only raise the running max and are streamed again at the end (fewer transient
 // candidates).  Each row list is split into four private quarters, one per thread of the row, so an
 // append is a plain shared store at a register counter (no atomics) and every thread's list keeps
-// the stream order: the iteration sums are formed in a fixed order and are bitwise reproducible
-// (entries appended under a racy, lower running threshold are <= τ_lo(m) and add exact zeros).  Overflow (a row list is finite): tier 1 streams K once more with the exact threshold
+// the stream order; the iteration sums are fixed-point (FxSum below), so τ is bitwise reproducible
+// (entries appended under a racy, lower running threshold are <= τ_lo(m) and add nothing).  Overflow (a row list is finite): tier 1 streams K once more with the exact threshold
 // τ_lo(m); tier 2, if even that overflows (wide supports, small α), streams T more passes over all
 // visible blocks — Alg. 3 itself.
 // Warp roles (576 threads): warps 0-15 math in four groups of four (thread t: row t & 127; group
@@ -55,6 +55,44 @@ __device__ __forceinline__ void list_append(uint32_t& as, uint32_t& aj, uint32_t
       : "+r"(as), "+r"(aj)
       : "f"(v), "f"(thr), "h"((unsigned short)tag), "r"(end)
       : "memory");
+}
+
+// Order-independent sums of Eqs. 3/6/7: every term is rounded once to fixed point and the integers
+// add exactly, so τ is bitwise the same whatever partition and order the contributing scores were
+// visited in — the online lists, the exact-threshold rebuild (tier 1) and the streaming passes (tier 2)
+// all give identical bits, and the (racy, timing-dependent) choice between them cannot change the
+// result.  E ∈ {1, 2, 4}: every term lies in [0, 1] (x <= m·c′ − τ_lo = 1), and its 2^-23 fixed-point
+// value is the mantissa of t + 1 (one FADD, exact RN rounding) — unit 2^-23.  Generic α: unit 2^-32 for
+// [x]_+^e, [x]_+^{e−1} ∈ [0, 1]; [x]_+^{e−2} exceeds 1 when e < 2 (α > 1.5): unit 2^-20, clamped at 2^30.
+struct FxSum {
+  unsigned long long q0, q1, q2;
+};
+__device__ __forceinline__ uint32_t fx23(float t) { return __float_as_uint(t + 1.0f) - 0x3f800000u; }
+// terms of one x into 32-bit partials (E != 0; x <= 0 gives zero terms and fx23(0) = 0 exactly;
+// <= 256 terms per partial)
+template <int E>
+__device__ __forceinline__ void accum_fx32(float x, const AlphaParams& ap, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
+  float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+  accum_f<E>(x, ap, t0, t1, t2);
+  p0 += fx23(t0);
+  p1 += fx23(t1);
+  p2 += fx23(t2);
+}
+template <int E>
+__device__ __forceinline__ void accum_fx(float x, const AlphaParams& ap, float u2, FxSum& q) {
+  if constexpr (E != 0) {
+    uint32_t p0 = 0, p1 = 0, p2 = 0;
+    accum_fx32<E>(x, ap, p0, p1, p2);
+    q.q0 += p0;
+    q.q1 += p1;
+    q.q2 += p2;
+  } else {
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+    accum_f<E>(x, ap, t0, t1, t2);
+    q.q0 += __float2ull_rn(t0 * 4294967296.0f);
+    q.q1 += __float2ull_rn(t1 * 4294967296.0f);
+    q.q2 += __float2ull_rn(fminf(t2, 1073741824.0f) * u2);
+  }
 }
 
 template <int D>
@@ -266,20 +304,27 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       return s_fallback != 0;
     };
 
-    // Σ over the row's four column quarters in a fixed order (every thread of the row gets the
-    // identical sums, so the four Alg. 1 updates agree bit for bit)
-    // (only the four warps that share the row's TMEM lane quadrant take part: barrier 2 + quadrant)
-    auto row_sum3 = [&](float& a0, float& a1, float& a2) {
+    // Σ of the row's four fixed-point partial sums (integer adds: exact, any order) → fp32 a0, a1, a2;
+    // only the four warps that share the row's TMEM lane quadrant take part (barrier 2 + quadrant)
+    // fixed-point units (FxSum): 2^-23 for E != 0; generic α 2^-32 (f, f') and u2 (f'')
+    const float u01 = E != 0 ? 8388608.0f : 4294967296.0f;
+    const float u2 = E != 0 ? 8388608.0f : (ap.em2 < 0.f ? 1048576.0f : 4294967296.0f);
+    auto row_sum3_fx = [&](const FxSum& q, float& a0, float& a1, float& a2) {
+      unsigned long long* x64 = reinterpret_cast<unsigned long long*>(xch);
       const uint32_t qbar = 2u + (uint32_t)(warp & 3);
       ptx::named_bar_sync(qbar, 128);
-      xch[tid] = a0;
-      xch[kTauMath + tid] = a1;
-      xch[2 * kTauMath + tid] = a2;
+      x64[tid] = q.q0;
+      x64[kTauMath + tid] = q.q1;
+      x64[2 * kTauMath + tid] = q.q2;
       ptx::named_bar_sync(qbar, 128);
-      a0 = (xch[r] + xch[128 + r]) + (xch[256 + r] + xch[384 + r]);
-      a1 = (xch[kTauMath + r] + xch[kTauMath + 128 + r]) + (xch[kTauMath + 256 + r] + xch[kTauMath + 384 + r]);
-      a2 = (xch[2 * kTauMath + r] + xch[2 * kTauMath + 128 + r]) +
-           (xch[2 * kTauMath + 256 + r] + xch[2 * kTauMath + 384 + r]);
+      const unsigned long long s0 = x64[r] + x64[128 + r] + x64[256 + r] + x64[384 + r];
+      const unsigned long long s1 =
+          x64[kTauMath + r] + x64[kTauMath + 128 + r] + x64[kTauMath + 256 + r] + x64[kTauMath + 384 + r];
+      const unsigned long long s2 = x64[2 * kTauMath + r] + x64[2 * kTauMath + 128 + r] +
+                                    x64[2 * kTauMath + 256 + r] + x64[2 * kTauMath + 384 + r];
+      a0 = (float)s0 * (1.0f / u01);
+      a1 = (float)s1 * (1.0f / u01);
+      a2 = (float)s2 * (1.0f / u2);
     };
 
     // this thread's private list: slots [qc·kCapQ, (qc+1)·kCapQ) of row r
@@ -400,8 +445,8 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
 
     if (!fallback) {
-      // ---- T iterations of Alg. 1 on the row lists: each thread sums its own list in stream order
-      // and the row's four quarters combine in a fixed order (row_sum3), so τ is bitwise reproducible.
+      // ---- T iterations of Alg. 1 on the row lists: fixed-point sums (FxSum), so τ is bitwise
+      // reproducible whichever path produced the lists.
       if (tid == 0) ENTMAX_TRACE_EV(8005);
       const int n = list_len();
       // the first kReg entries live in registers for all T iterations (−∞ pads contribute zeros)
@@ -410,13 +455,29 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 #pragma unroll
       for (int c = 0; c < kReg; ++c) lr[c] = c < n ? ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u) : -INFINITY;
       for (int t = 0; t < n_iter; ++t) {
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        FxSum q{0ull, 0ull, 0ull};
+        if constexpr (E != 0) {   // <= kCapQ (< 256) terms per thread: 32-bit partials
+          uint32_t p0 = 0, p1 = 0, p2 = 0;
 #pragma unroll
-        for (int c = 0; c < kReg; ++c) accum_f<E>(fmaf(lr[c], ap.cp, -rs.tau), ap, a0, a1, a2);
+          for (int c = 0; c < kReg; ++c) accum_fx32<E>(fmaf(lr[c], ap.cp, -rs.tau), ap, p0, p1, p2);
 #pragma unroll 4
-        for (int c = kReg; c < n; ++c)
-          accum_f<E>(fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau), ap, a0, a1, a2);
-        row_sum3(a0, a1, a2);
+          for (int c = kReg; c < n; ++c)
+            accum_fx32<E>(fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau), ap, p0, p1, p2);
+          q = FxSum{p0, p1, p2};
+        } else {
+#pragma unroll
+          for (int c = 0; c < kReg; ++c) {
+            const float x = fmaf(lr[c], ap.cp, -rs.tau);
+            if (x > 0.f) accum_fx<E>(x, ap, u2, q);
+          }
+#pragma unroll 4
+          for (int c = kReg; c < n; ++c) {
+            const float x = fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau);
+            if (x > 0.f) accum_fx<E>(x, ap, u2, q);
+          }
+        }
+        float a0, a1, a2;
+        row_sum3_fx(q, a0, a1, a2);
         alg1_update(rs, a0, a1, a2, ap);
       }
       if (tid == 0) ENTMAX_TRACE_EV(8008);
@@ -458,7 +519,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         }
       }
       for (int it = 0; it < n_iter; ++it) {
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        FxSum q{0ull, 0ull, 0ull};
         for (int t = first_t(kglob); t < nkb; t += kTauSBuf) {
           wait_tile(kglob + t);
 #pragma unroll 1
@@ -469,13 +530,26 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 #pragma unroll
             for (int e = 1; e < 31; e += 2) cm = fmax3(cm, s[e], s[e + 1]);
             if (__any_sync(0xffffffffu, fmaf(cm, ap.cp, -rs.tau) > 0.f)) {
+              if constexpr (E != 0) {   // 32 terms per chunk: 32-bit partials, widened once
+                uint32_t p0 = 0, p1 = 0, p2 = 0;
 #pragma unroll
-              for (int e = 0; e < 32; ++e) accum_f<E>(fmaf(s[e], ap.cp, -rs.tau), ap, a0, a1, a2);
+                for (int e = 0; e < 32; ++e) accum_fx32<E>(fmaf(s[e], ap.cp, -rs.tau), ap, p0, p1, p2);
+                q.q0 += p0;
+                q.q1 += p1;
+                q.q2 += p2;
+              } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                  const float x = fmaf(s[e], ap.cp, -rs.tau);
+                  if (x > 0.f) accum_fx<E>(x, ap, u2, q);
+                }
+              }
             }
           }
         }
         kglob += nkb;
-        row_sum3(a0, a1, a2);
+        float a0, a1, a2;
+        row_sum3_fx(q, a0, a1, a2);
         alg1_update(rs, a0, a1, a2, ap);
       }
       if (qc == 0 && valid) tau_out[(long long)bh * g.N + row] = rs.tau;

@@ -1,0 +1,18 @@
+"""Small fwd+bwd cases for compute-sanitizer runs (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2502_12082_b200 as P
+from tests.parity import make_case
+for (B, H, N, d, dt, causal) in [(1, 2, 300, 64, torch.bfloat16, True), (1, 1, 384, 128, torch.bfloat16, False),
+                                 (1, 1, 200, 64, torch.float32, True)]:
+    dev, _ = make_case(B, H, N, d, dt, seed=3)
+    q, k, v, do = dev
+    for masked in (True, False):
+        fw = P.entmax_attn_fwd(q, k, v, 1.5, causal, 3, masked=masked)
+        P.entmax_attn_bwd(q, k, v, do, fw, 1.5, causal)
+p, t = P.entmax_rowwise_fwd(torch.randn(8, 1000, device="cuda"), 1.5, 3)
+P.entmax_rowwise_bwd(p, torch.randn_like(p), 1.5)
+p, t = P.entmax_rowwise_fwd(torch.randn(4, 20000, device="cuda"), 1.5, 23, halley=False)
+torch.cuda.synchronize()
+print("sanitize case ok")
