@@ -351,9 +351,9 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       for (int t = first_t(kglob); t < nsteps; t += kTauSBuf) {
         const int j = t < nkb ? t : t - nkb;
         wait_tile(kglob + t);
-        const float mread = online ? ptx::ld_shared_f32(msh) : 0.f;   // once per tile
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
+          const float mread = online ? ptx::ld_shared_f32(msh) : 0.f;   // the row's published max
           float s[32];
           read_chunk(j, c, s);
           float gm[4];
