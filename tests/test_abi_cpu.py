@@ -105,3 +105,16 @@ def test_rowwise_bwd_rejects_misaligned_pointer():
     rc = L.entmax_rowwise_bwd(ctypes.c_void_p(0x10004), ctypes.c_void_p(0x10000), 2, 64, 64, 1, 1.5,
                               ctypes.c_void_p(0x10000), None)
     assert rc == 1
+
+
+def test_unmasked_mode_partial_null_tables_rejected_before_launch():
+    """mask / row_cnt / row_idx must be all set or all NULL (unmasked mode, NEXT-2)."""
+    L = _lib.lib()
+    s = _lib.Shape(1, 1, 256, 64, 256 * 64, 256 * 64, 64)
+    fake = ctypes.c_void_p(0x10000)
+    rc = L.entmax_attn_fwd(fake, fake, fake, ctypes.byref(s), 0, 1.5, 0, 3, 0.0,
+                           fake, fake, fake, fake, None, fake, fake, 1 << 30, None)
+    assert rc == 1 and b"all NULL" in L.entmax_attn_last_error()
+    rc = L.entmax_attn_bwd(fake, fake, fake, fake, fake, fake, None, fake, None, ctypes.byref(s), 0, 1.5, 0, 0.0,
+                           fake, fake, fake, fake, 1 << 30, None)
+    assert rc == 1 and b"all NULL" in L.entmax_attn_last_error()
