@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 
 #include "entmax_rowwise.h"
 #include "common.cuh"
@@ -362,11 +363,19 @@ __global__ void __launch_bounds__(kStreamNT) bwd_stream_kernel(const T* p, const
 // Register-path shapes (NT threads × VPT values): chosen by n so a CTA holds its whole row.
 template <typename T, int E, typename Op>
 int by_n(int n, Op&& op) {
+  // (NT, VPT) measured on 8192 × {4096, 8192, 16384} rows: few threads per row (cheap block
+  // reductions) with 32 values each for fp32, 64 for bf16 (same bytes per thread); longer rows take
+  // more threads, then the streaming variant
   constexpr int W = Chunk<T>::W;
   if (n <= 128 * 2 * W) return op.template run<128, 2 * W>();
-  if (n <= 256 * 4 * W) return op.template run<256, 4 * W>();
-  if (n <= 256 * 32) return op.template run<256, 32>();
-  if (n <= 512 * 32) return op.template run<512, 32>();
+  if (n <= 128 * 32) return op.template run<128, 32>();
+  if constexpr (W == 8) {
+    if (n <= 128 * 64) return op.template run<128, 64>();
+    if (n <= 256 * 64) return op.template run<256, 64>();
+  } else {
+    if (n <= 256 * 32) return op.template run<256, 32>();
+    if (n <= 512 * 32) return op.template run<512, 32>();
+  }
   return op.template run<0, 0>();   // streaming
 }
 
@@ -419,17 +428,23 @@ int by_n_bwd(int n, Op&& op) {
   if (n <= 128 * 2 * W) return op.template run<128, 2 * W>();
   if (n <= 1024 * W) return op.template run<1024, W>();
   if (n <= 1024 * 2 * W) return op.template run<1024, 2 * W>();
-  if (n <= 1024 * 4 * W) return op.template run<1024, 4 * W>();
+  if (n <= 1024 * 16) return op.template run<1024, 16>();   // (<= 64 registers at 1024 threads)
   return op.template run<0, 0>();   // streaming
 }
 
 template <template <typename, int> class L, typename T, bool BWD, typename... A>
 int by_e(int ecode, int n, A... a) {
+  auto go = [n](auto&& op) {
+    using Op = std::decay_t<decltype(op)>;
+    if constexpr (BWD) return by_n_bwd<T, 0>(n, op);
+    else return by_n<T, 0>(n, op);
+    (void)sizeof(Op);
+  };
   switch (ecode) {
-    case 1: { L<T, 1> op{a...}; return BWD ? by_n_bwd<T, 1>(n, op) : by_n<T, 1>(n, op); }
-    case 2: { L<T, 2> op{a...}; return BWD ? by_n_bwd<T, 2>(n, op) : by_n<T, 2>(n, op); }
-    case 4: { L<T, 4> op{a...}; return BWD ? by_n_bwd<T, 4>(n, op) : by_n<T, 4>(n, op); }
-    default: { L<T, 0> op{a...}; return BWD ? by_n_bwd<T, 0>(n, op) : by_n<T, 0>(n, op); }
+    case 1: return go(L<T, 1>{a...});
+    case 2: return go(L<T, 2>{a...});
+    case 4: return go(L<T, 4>{a...});
+    default: return go(L<T, 0>{a...});
   }
 }
 
