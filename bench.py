@@ -238,10 +238,18 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         world = max(world, 1)
+    # ENTMAX_BENCH_SHARE_GPU=1 / ENTMAX_BENCH_BACKEND=gloo: test hook to exercise the multi-rank path
+    # on a one-GPU box (ranks share cuda:0, gloo carries the barriers and the max-over-ranks timing)
+    if os.environ.get("ENTMAX_BENCH_SHARE_GPU") == "1":
+        local = local % torch.cuda.device_count()
+    backend = os.environ.get("ENTMAX_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     B, H, N, d = cfg["B"], cfg["H"], cfg["N"], cfg["d"]
     spec = synth.HeadSpec(cfg["gen"], rho=cfg["rho"])
@@ -279,7 +287,7 @@ def main():
             dist.barrier()
         ms = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms / steps
@@ -352,7 +360,7 @@ def main():
             dist.barrier()
         ms = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms / steps
