@@ -24,6 +24,25 @@ struct ProfScope {
   ~ProfScope();
 };
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while the previous
+// kernel of the stream drains; every kernel so launched calls griddepcontrol.wait before it touches
+// global data (sm100_ptx.cuh griddep_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // SIMT path (simt.cu)
 int simt_fwd_launch(int dtype, int d, int ecode, const void* q, const void* k, const void* v, const Geom& g,
                     const AlphaParams& ap, int n_iter, void* o, void* o2, float* tau, uint8_t* mask,

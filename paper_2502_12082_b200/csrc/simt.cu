@@ -101,10 +101,10 @@ static void delta_go(const T* dO, const float* o2, const Geom& g, float* delta, 
   const int tpr = g.d / 8;
   const unsigned blocks = (unsigned)((rows * tpr + 255) / 256);
   switch (tpr) {
-    case 2: delta_kernel<T, 2><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
-    case 4: delta_kernel<T, 4><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
-    case 8: delta_kernel<T, 8><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
-    default: delta_kernel<T, 16><<<blocks, 256, 0, st>>>(dO, o2, g, delta); break;
+    case 2: launch_pdl(delta_kernel<T, 2>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
+    case 4: launch_pdl(delta_kernel<T, 4>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
+    case 8: launch_pdl(delta_kernel<T, 8>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
+    default: launch_pdl(delta_kernel<T, 16>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
   }
 }
 
@@ -124,7 +124,8 @@ int col_lists_launch(const uint8_t* mask, const Geom& g, int32_t* col_cnt, int32
   const long long n = (long long)g.B * g.H * g.Tc;
   {
     ProfScope ps("col_lists", st);
-    col_lists_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(mask, g.B * g.H, g.Tr, g.Tc, col_cnt, col_idx);
+    launch_pdl(col_lists_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, mask, g.B * g.H, g.Tr, g.Tc,
+               col_cnt, col_idx);
   }
   return cuda_status("col_lists");
 }

@@ -318,6 +318,8 @@ __device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
 template <typename T, int TPR>
 __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, const float* __restrict__ o2, Geom g,
                                                     float* __restrict__ delta) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // (launched with PDL: see runtime.h)
   const long long row = ((long long)blockIdx.x * 256 + threadIdx.x) / TPR;
   const int sub = threadIdx.x % TPR;
   const long long total = (long long)g.B * g.H * g.N;
@@ -340,6 +342,8 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, co
 // 𝒦_j = {i | M_ij = 1} from the mask, increasing i; one thread per (head, j).
 __global__ void col_lists_kernel(const uint8_t* __restrict__ mask, int BH, int Tr, int Tc,
                                  int32_t* __restrict__ col_cnt, int32_t* __restrict__ col_idx) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // (launched with PDL: see runtime.h)
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)BH * Tc) return;
   const int bh = (int)(t / Tc), j = (int)(t - (long long)(t / Tc) * Tc);

@@ -53,21 +53,24 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
     const size_t sm = TauSmem<D>::bytes(g.Tc);
     if (int rc = set_smem(tau_kernel<D, E>, sm)) return rc;
     ProfScope ps("tau_sm100", st);
-    tau_kernel<D, E><<<dim3((g.Tr + 1) & ~1, g.B * g.H), kTauThreads, sm, st>>>(tq, tk64, g, ap, n_iter, tau, cand_cnt,
-                                                                               cand_idx);
+    if (cudaError_t e = launch_pdl(tau_kernel<D, E>, dim3((g.Tr + 1) & ~1, g.B * g.H), dim3(kTauThreads), sm, st, tq,
+                                   tk64, g, ap, n_iter, tau, cand_cnt, cand_idx))
+      return fail(ENTMAX_ERR_CUDA, "tau_sm100 launch: %s", cudaGetErrorString(e));
   }
   if (int rc = cuda_status("tau_sm100")) return rc;
   const size_t sm = out_smem<D>(g.Tc);
   if (o2 != nullptr) {
     if (int rc = set_smem(out_kernel<D, E, true>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    out_kernel<D, E, true><<<grid, kFbThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
-                                                       (__nv_bfloat16*)o, (float*)o2, mask, row_cnt, row_idx);
+    if (cudaError_t e = launch_pdl(out_kernel<D, E, true>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
+                                   cand_cnt, cand_idx, (__nv_bfloat16*)o, (float*)o2, mask, row_cnt, row_idx))
+      return fail(ENTMAX_ERR_CUDA, "out_sm100 launch: %s", cudaGetErrorString(e));
   } else {
     if (int rc = set_smem(out_kernel<D, E, false>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    out_kernel<D, E, false><<<grid, kFbThreads, sm, st>>>(tq, tk, tv, g, ap, tau, cand_cnt, cand_idx,
-                                                        (__nv_bfloat16*)o, nullptr, mask, row_cnt, row_idx);
+    if (cudaError_t e = launch_pdl(out_kernel<D, E, false>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
+                                   cand_cnt, cand_idx, (__nv_bfloat16*)o, (float*)nullptr, mask, row_cnt, row_idx))
+      return fail(ENTMAX_ERR_CUDA, "out_sm100 launch: %s", cudaGetErrorString(e));
   }
   return cuda_status("out_sm100");
 }
@@ -82,16 +85,18 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
     const size_t sm = dkdv_smem<D>();
     if (int rc = set_smem(dkdv_kernel<D, E>, sm)) return rc;
     ProfScope ps("dkdv_sm100", st);
-    dkdv_kernel<D, E><<<dim3(g.Tc, g.B * g.H), kFbThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, col_cnt,
-                                                                     col_idx, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv);
+    if (cudaError_t e = launch_pdl(dkdv_kernel<D, E>, dim3(g.Tc, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo,
+                                   g, ap, tau, delta, col_cnt, col_idx, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
+      return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
   }
   if (int rc = cuda_status("dkdv_sm100")) return rc;
   {
     const size_t sm = dq_smem<D>();
     if (int rc = set_smem(dq_kernel<D, E>, sm)) return rc;
     ProfScope ps("dq_sm100", st);
-    dq_kernel<D, E><<<dim3(g.Tr, g.B * g.H), kFbThreads, sm, st>>>(tq, tk, tv, tdo, g, ap, tau, delta, row_cnt, row_idx,
-                                                                   (__nv_bfloat16*)dq);
+    if (cudaError_t e = launch_pdl(dq_kernel<D, E>, dim3(g.Tr, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo, g,
+                                   ap, tau, delta, row_cnt, row_idx, (__nv_bfloat16*)dq))
+      return fail(ENTMAX_ERR_CUDA, "dq_sm100 launch: %s", cudaGetErrorString(e));
   }
   return cuda_status("dq_sm100");
 }

@@ -105,9 +105,6 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long li = (long long)bh * g.Tr + i;
-  const bool dense = mask == nullptr;   // unmasked mode: every visible block, no mask / table output
-  const int ncand = dense ? g.visible_kblocks(i) : cand_cnt[li];
-  const BlockList list{dense ? nullptr : cand_idx + li * g.Tc, 0};
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
@@ -129,6 +126,11 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t t_o = tmem + 256, t_o2 = tmem + 256 + D;
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();   // the τ kernel's outputs are complete and visible
+  const bool dense = mask == nullptr;   // unmasked mode: every visible block, no mask / table output
+  const int ncand = dense ? g.visible_kblocks(i) : cand_cnt[li];
+  const BlockList list{dense ? nullptr : cand_idx + li * g.Tc, 0};
 
   if (warp == 8) {
     ptx::tma_prefetch_desc(&tq);
@@ -290,9 +292,6 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5;
   const long long li = (long long)bh * g.Tr + i;
-  const bool dense = row_idx == nullptr;   // unmasked mode: every visible key block
-  const int cnt = dense ? g.visible_kblocks(i) : row_cnt[li];
-  const BlockList list{dense ? nullptr : row_idx + li * g.Tc, 0};
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
@@ -313,6 +312,11 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_ds = tmem + 256, t_dq = tmem + 320;
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();   // the dK/dV kernel (and everything before it) is complete
+  const bool dense = row_idx == nullptr;   // unmasked mode: every visible key block
+  const int cnt = dense ? g.visible_kblocks(i) : row_cnt[li];
+  const BlockList list{dense ? nullptr : row_idx + li * g.Tc, 0};
 
   if (warp == 8) {
     ptx::tma_prefetch_desc(&tk);
@@ -447,10 +451,6 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long lj = (long long)bh * g.Tc + j;
-  const bool dense = col_idx == nullptr;   // unmasked mode: every query block that sees key block j
-  const int i0 = g.causal ? (j * kBc) / kBr : 0;
-  const int cnt = dense ? g.Tr - i0 : col_cnt[lj];
-  const BlockList list{dense ? nullptr : col_idx + lj * g.Tr, i0};
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_kv, 1);
@@ -471,6 +471,12 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const uint32_t t_s = tmem, t_dp = tmem + 128;
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();   // δ and the 𝒦 tables are complete
+  const bool dense = col_idx == nullptr;   // unmasked mode: every query block that sees key block j
+  const int i0 = g.causal ? (j * kBc) / kBr : 0;
+  const int cnt = dense ? g.Tr - i0 : col_cnt[lj];
+  const BlockList list{dense ? nullptr : col_idx + lj * g.Tr, i0};
   const uint32_t t_dv = tmem + (ALIAS ? 256 : 384), t_dk = t_dv + D;
   auto pt_col = [&](int ks) { return ALIAS ? t_s + 8 * ks + (ks >= 4 ? 32 : 0) : tmem + 256 + 8 * ks; };
   auto dst_col = [&](int ks) { return ALIAS ? t_dp + 8 * ks + (ks >= 4 ? 32 : 0) : tmem + 320 + 8 * ks; };

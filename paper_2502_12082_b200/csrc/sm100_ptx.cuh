@@ -400,6 +400,14 @@ __device__ __forceinline__ uint32_t ld_shared_u16(uint32_t saddr) {
   return v;
 }
 
+// Programmatic dependent launch (the kernels are launched with programmatic stream serialization):
+// let the next kernel of the stream start its prologue on SMs this grid frees, and wait for the
+// previous kernel's completion (and memory) before touching global data it produces or consumes.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -178,6 +178,8 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   ptx::cluster_sync();   // both CTAs' barriers exist before any multicast targets them
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();   // the previous kernel (e.g. last step's dQ reading τ) is complete
 
   if (warp == kTauMathWarps) {
     // ---------------------------------------------------------------- TMA producer
