@@ -6,9 +6,10 @@ current CUDA stream and autograd plumbing only.  There is no CPU/eager fallback:
 library or a CUDA device is missing the calls raise.
 
 Public API (same names as the C ABI):
-  entmax_attn_fwd(q, k, v, alpha, causal, n_iter, scale=None, training=True) -> FwdResult
+  entmax_attn_fwd(q, k, v, alpha, causal, n_iter, scale=None, training=True, masked=True) -> FwdResult
   entmax_attn_bwd(q, k, v, d_o, fwd: FwdResult, alpha, causal, scale=None) -> (dq, dk, dv)
-  entmax_attention(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None)  (autograd op)
+  entmax_attention(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, masked=True)  (autograd op)
+    masked=False: the paper's unmasked variant (every visible block, no mask / lookup tables).
   entmax_rowwise_fwd(s, alpha, n_iter, halley=True) -> (p, tau)    (include/entmax_rowwise.h)
   entmax_rowwise_bwd(p, dp, alpha) -> ds
   entmax(s, alpha=1.5, n_iter=3, halley=True)  (autograd op over the last dimension)
