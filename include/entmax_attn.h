@@ -26,7 +26,8 @@
  *    increasing j, padded (ELL).  Causal: key j′ is visible to query i′ iff j′ <= i′.
  *  - Ownership: the caller allocates every buffer (including the workspace, sized by the
  *    *_workspace_bytes queries) and keeps it alive until the stream work completes.  The
- *    library allocates no device memory and keeps no per-call state.
+ *    library allocates no device memory and keeps no per-call state, so one workspace can be
+ *    shared by every layer / call on a stream.
  *  - Asynchrony: all work is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
  *    legacy default stream).  No host synchronisation happens inside the calls.
  *  - Errors: every function returns an entmax_status_t; nothing is thrown across the ABI.
@@ -116,6 +117,14 @@ int entmax_attn_bwd(const void* q, const void* k, const void* v, const void* o2,
                     const float* tau, const uint8_t* mask, const int32_t* row_cnt, const int32_t* row_idx,
                     const entmax_shape_t* shp, int dtype, float alpha, int causal, float scale,
                     void* dq, void* dk, void* dv, void* workspace, size_t ws_bytes, void* stream);
+
+/*
+ * Bit-packed block mask: out[r, w] bit b = mask[r, 32·w + b] != 0 for the rows
+ * r < rows (= B·H·T_r) of a [rows, T_c] uint8 mask; out is [rows, ⌈T_c/32⌉] uint32, bits past T_c
+ * zero.  8× smaller than the byte mask for callers that keep masks across layers or steps.
+ * Device pointers; asynchronous on `stream`; INVALID_ARG for NULL pointers or rows/Tc < 1.
+ */
+int entmax_attn_pack_mask(const uint8_t* mask, int64_t rows, int32_t Tc, uint32_t* out, void* stream);
 
 /*
  * Kernel timing (instrumentation for bench.py's roofline numbers; off by default).

@@ -28,7 +28,7 @@ from ._lib import EntmaxAttnError, ENTMAX_BF16, ENTMAX_FP32
 
 __all__ = ["entmax_attn_fwd", "entmax_attn_bwd", "entmax_attention", "block_size", "FwdResult",
            "EntmaxAttnError", "impl_for", "profile_enable", "profile_reset", "profile_collect",
-           "workspace_bytes", "entmax_rowwise_fwd", "entmax_rowwise_bwd", "entmax"]
+           "workspace_bytes", "entmax_rowwise_fwd", "entmax_rowwise_bwd", "entmax", "pack_mask"]
 
 _DT = {torch.bfloat16: ENTMAX_BF16, torch.float32: ENTMAX_FP32}
 
@@ -263,3 +263,16 @@ class _Entmax(torch.autograd.Function):
 def entmax(s, alpha=1.5, n_iter=3, halley=True):
     """α-entmax over the last dimension (Eq. 2) by Halley-bisection (autograd op)."""
     return _Entmax.apply(s, alpha, n_iter, halley)
+
+
+def pack_mask(mask: torch.Tensor) -> torch.Tensor:
+    """Bit-packed block mask [..., T_r, ⌈T_c/32⌉] int32 (bit b of word w = M[..., 32w + b])."""
+    if not mask.is_cuda or mask.dtype != torch.uint8:
+        raise ValueError("mask must be a CUDA uint8 tensor")
+    m = mask.contiguous()
+    Tc = m.shape[-1]
+    rows = m.numel() // Tc
+    out = torch.empty(m.shape[:-1] + (-(-Tc // 32),), dtype=torch.int32, device=m.device)
+    _lib.check(_lib.lib().entmax_attn_pack_mask(_ptr(m), rows, Tc, _ptr(out), _stream(m.device)),
+               "entmax_attn_pack_mask")
+    return out

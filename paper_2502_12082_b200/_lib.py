@@ -68,6 +68,8 @@ def lib() -> ctypes.CDLL:
     L.entmax_attn_impl_for.restype = i32
     L.entmax_attn_impl_for.argtypes = [pshape, i32]
     i64 = ctypes.c_int64
+    L.entmax_attn_pack_mask.restype = i32
+    L.entmax_attn_pack_mask.argtypes = [vp, i64, ctypes.c_int32, vp, vp]
     L.entmax_rowwise_fwd.restype = i32          # include/entmax_rowwise.h
     L.entmax_rowwise_fwd.argtypes = [vp, i64, ctypes.c_int32, i64, i32, f32, i32, i32, vp, vp, vp]
     L.entmax_rowwise_bwd.restype = i32

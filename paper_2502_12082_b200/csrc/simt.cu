@@ -131,3 +131,13 @@ int col_lists_launch(const uint8_t* mask, const Geom& g, int32_t* col_cnt, int32
 }
 
 }  // namespace entmax
+
+extern "C" int entmax_attn_pack_mask(const uint8_t* mask, int64_t rows, int32_t Tc, uint32_t* out, void* stream) {
+  using namespace entmax;
+  if (!mask || !out) return fail(ENTMAX_ERR_INVALID_ARG, "NULL pointer");
+  if (rows < 1 || Tc < 1) return fail(ENTMAX_ERR_INVALID_ARG, "rows and Tc must be >= 1");
+  const int words = (Tc + 31) / 32;
+  const long long n = rows * words;
+  pack_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(mask, rows, Tc, words, out);
+  return cuda_status("pack_mask");
+}

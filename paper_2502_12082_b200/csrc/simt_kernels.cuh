@@ -355,4 +355,18 @@ __global__ void col_lists_kernel(const uint8_t* __restrict__ mask, int BH, int T
   col_cnt[t] = cnt;
 }
 
+// bit-packed mask: one thread per output word (32 mask bytes)
+__global__ void pack_mask_kernel(const uint8_t* __restrict__ mask, long long rows, int Tc, int words,
+                                 uint32_t* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * words) return;
+  const long long r = t / words;
+  const int w = (int)(t - r * words);
+  const uint8_t* m = mask + r * Tc + w * 32;
+  const int nb = min(32, Tc - w * 32);
+  uint32_t v = 0;
+  for (int b = 0; b < nb; ++b) v |= (m[b] != 0 ? 1u : 0u) << b;
+  out[t] = v;
+}
+
 }  // namespace entmax

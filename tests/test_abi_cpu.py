@@ -118,3 +118,9 @@ def test_unmasked_mode_partial_null_tables_rejected_before_launch():
     rc = L.entmax_attn_bwd(fake, fake, fake, fake, fake, fake, None, fake, None, ctypes.byref(s), 0, 1.5, 0, 0.0,
                            fake, fake, fake, fake, 1 << 30, None)
     assert rc == 1 and b"all NULL" in L.entmax_attn_last_error()
+
+
+def test_pack_mask_validation():
+    L = _lib.lib()
+    assert L.entmax_attn_pack_mask(None, 4, 8, ctypes.c_void_p(0x10000), None) == 1
+    assert L.entmax_attn_pack_mask(ctypes.c_void_p(0x10000), 0, 8, ctypes.c_void_p(0x10000), None) == 1

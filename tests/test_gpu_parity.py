@@ -2,6 +2,7 @@
 
 Sizes span several 128×128 tiles and ragged tails; the oracle finishes each in seconds.
 """
+import numpy as np
 import pytest
 import torch
 
@@ -236,3 +237,19 @@ def test_repeated_runs_bitwise_identical(gen, N, alpha, causal):
         else:
             for a, b in zip(cur, ref):
                 assert torch.equal(a, b)
+
+
+def test_pack_mask_bits():
+    """Bit-packed M (NEXT-2): bit b of word w of row r equals M[r, 32w + b]; padding bits zero."""
+    _require_gpu()
+    import paper_2502_12082_b200 as P
+    g = torch.Generator().manual_seed(0)
+    for Tc in (1, 31, 32, 33, 64, 100):
+        m = (torch.rand(3, 5, 7, Tc, generator=g) < 0.4).to(torch.uint8)
+        pk = P.pack_mask(m.cuda()).cpu().numpy().astype(np.uint32)
+        mm = m.numpy()
+        for w in range(pk.shape[-1]):
+            for b in range(32):
+                col = 32 * w + b
+                want = mm[..., col] if col < Tc else np.zeros(mm.shape[:-1], np.uint8)
+                assert np.array_equal((pk[..., w] >> b) & 1, want.astype(np.uint32))
