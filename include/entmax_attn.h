@@ -49,7 +49,7 @@ extern "C" {
 typedef enum {
   ENTMAX_OK = 0,
   ENTMAX_ERR_INVALID_ARG = 1,  /* bad shape, α < 1+1e-3, n_iter < 1, null/misaligned pointer */
-  ENTMAX_ERR_UNSUPPORTED = 2,  /* α > 2, head dim not supported by any kernel              */
+  ENTMAX_ERR_UNSUPPORTED = 2,  /* α > 2, head dim not supported, B·H > 65535, N > 2^24       */
   ENTMAX_ERR_WORKSPACE = 3,    /* workspace smaller than the *_workspace_bytes query      */
   ENTMAX_ERR_CUDA = 4          /* a CUDA launch failed                                    */
 } entmax_status_t;

@@ -93,6 +93,9 @@ int check_shape(const entmax_shape_t* s, int dtype) {
   if ((s->sn * esz) % 16 || (s->sh * esz) % 16 || (s->sb * esz) % 16 || (s->d * esz) % 16)
     return fail(ENTMAX_ERR_INVALID_ARG, "strides and d must be multiples of 16 bytes");
   if ((int64_t)s->N * 1 > (1 << 24)) return fail(ENTMAX_ERR_UNSUPPORTED, "N > 2^24 not supported");
+  if ((int64_t)s->B * s->H > 65535)   // heads are the grid's y dimension
+    return fail(ENTMAX_ERR_UNSUPPORTED, "B*H = %lld > 65535 heads per call: split the batch",
+                (long long)s->B * s->H);
   return ENTMAX_OK;
 }
 

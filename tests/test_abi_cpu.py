@@ -124,3 +124,12 @@ def test_pack_mask_validation():
     L = _lib.lib()
     assert L.entmax_attn_pack_mask(None, 4, 8, ctypes.c_void_p(0x10000), None) == 1
     assert L.entmax_attn_pack_mask(ctypes.c_void_p(0x10000), 0, 8, ctypes.c_void_p(0x10000), None) == 1
+
+
+def test_too_many_heads_rejected_before_launch():
+    L = _lib.lib()
+    s = _lib.Shape(70000, 1, 128, 64, 128 * 64, 128 * 64, 64)
+    fake = ctypes.c_void_p(0x10000)
+    rc = L.entmax_attn_fwd(fake, fake, fake, ctypes.byref(s), 0, 1.5, 0, 3, 0.0,
+                           fake, fake, fake, fake, fake, fake, fake, 1 << 40, None)
+    assert rc == 2 and b"65535" in L.entmax_attn_last_error()
