@@ -40,7 +40,7 @@ int tmaps(const Geom& g, std::initializer_list<std::pair<CUtensorMap*, const voi
   return ENTMAX_OK;
 }
 
-template <int D, int E>
+template <int D, int E, bool CU>
 int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const AlphaParams& ap, int n_iter, void* o,
           void* o2, float* tau, uint8_t* mask, int32_t* row_cnt, int32_t* row_idx, int32_t* cand_cnt,
           int32_t* cand_idx, cudaStream_t st) {
@@ -60,22 +60,22 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
   if (int rc = cuda_status("tau_sm100")) return rc;
   const size_t sm = out_smem<D>(g.Tc);
   if (o2 != nullptr) {
-    if (int rc = set_smem(out_kernel<D, E, true>, sm)) return rc;
+    if (int rc = set_smem(out_kernel<D, E, true, CU>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    if (cudaError_t e = launch_pdl(out_kernel<D, E, true>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
+    if (cudaError_t e = launch_pdl(out_kernel<D, E, true, CU>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
                                    cand_cnt, cand_idx, (__nv_bfloat16*)o, (float*)o2, mask, row_cnt, row_idx))
       return fail(ENTMAX_ERR_CUDA, "out_sm100 launch: %s", cudaGetErrorString(e));
   } else {
-    if (int rc = set_smem(out_kernel<D, E, false>, sm)) return rc;
+    if (int rc = set_smem(out_kernel<D, E, false, CU>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    if (cudaError_t e = launch_pdl(out_kernel<D, E, false>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
+    if (cudaError_t e = launch_pdl(out_kernel<D, E, false, CU>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
                                    cand_cnt, cand_idx, (__nv_bfloat16*)o, (float*)nullptr, mask, row_cnt, row_idx))
       return fail(ENTMAX_ERR_CUDA, "out_sm100 launch: %s", cudaGetErrorString(e));
   }
   return cuda_status("out_sm100");
 }
 
-template <int D, int E>
+template <int D, int E, bool CU>
 int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap,
           const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx,
           const int32_t* col_cnt, const int32_t* col_idx, void* dq, void* dk, void* dv, cudaStream_t st) {
@@ -83,18 +83,18 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
   {
     const size_t sm = dkdv_smem<D>();
-    if (int rc = set_smem(dkdv_kernel<D, E>, sm)) return rc;
+    if (int rc = set_smem(dkdv_kernel<D, E, CU>, sm)) return rc;
     ProfScope ps("dkdv_sm100", st);
-    if (cudaError_t e = launch_pdl(dkdv_kernel<D, E>, dim3(g.Tc, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo,
+    if (cudaError_t e = launch_pdl(dkdv_kernel<D, E, CU>, dim3(g.Tc, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo,
                                    g, ap, tau, delta, col_cnt, col_idx, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
       return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
   }
   if (int rc = cuda_status("dkdv_sm100")) return rc;
   {
     const size_t sm = dq_smem<D>();
-    if (int rc = set_smem(dq_kernel<D, E>, sm)) return rc;
+    if (int rc = set_smem(dq_kernel<D, E, CU>, sm)) return rc;
     ProfScope ps("dq_sm100", st);
-    if (cudaError_t e = launch_pdl(dq_kernel<D, E>, dim3(g.Tr, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo, g,
+    if (cudaError_t e = launch_pdl(dq_kernel<D, E, CU>, dim3(g.Tr, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo, g,
                                    ap, tau, delta, row_cnt, row_idx, (__nv_bfloat16*)dq))
       return fail(ENTMAX_ERR_CUDA, "dq_sm100 launch: %s", cudaGetErrorString(e));
   }
@@ -116,15 +116,20 @@ int dispatch(int d, int ecode, A&&... a) {
   return fail(ENTMAX_ERR_UNSUPPORTED, "tcgen05 path supports d in {64, 128} (got %d)", d);
 }
 
+// (the first argument after the inputs is the Geom: short rows select the consistent-Û kernels, r9)
 template <int D, int E>
 struct FwdOp {
-  template <typename... A>
-  static int run(A&&... a) { return fwd_t<D, E>(a...); }
+  template <typename Q, typename K, typename V, typename... A>
+  static int run(Q q, K k, V v, const Geom& g, A&&... a) {
+    return g.N <= kConsistentUMaxN ? fwd_t<D, E, true>(q, k, v, g, a...) : fwd_t<D, E, false>(q, k, v, g, a...);
+  }
 };
 template <int D, int E>
 struct BwdOp {
-  template <typename... A>
-  static int run(A&&... a) { return bwd_t<D, E>(a...); }
+  template <typename Q, typename K, typename V, typename O, typename... A>
+  static int run(Q q, K k, V v, O dO, const Geom& g, A&&... a) {
+    return g.N <= kConsistentUMaxN ? bwd_t<D, E, true>(q, k, v, dO, g, a...) : bwd_t<D, E, false>(q, k, v, dO, g, a...);
+  }
 };
 
 }  // namespace

@@ -19,6 +19,21 @@
 namespace entmax {
 namespace sm100 {
 
+// CU (consistent Û, reading r9): short rows (N <= kConsistentUMaxN) sum ‖Û‖₁ from the bf16-rounded U
+// the U·V MMA sees and form dS = Û ⊙ (dP − δ) from the same rounded Û, so Σ_j dS_ij = 0 holds without
+// a 2⁻⁹ mismatch (which does not average out over a 2-3 key support); long rows keep fp32 U.
+constexpr int kConsistentUMaxN = 512;
+// bf16x2 word → two floats; and a float2 rounded to bf16 (RN) and back
+__device__ __forceinline__ float2 bf16x2_to_float2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+// dS = Û ⊙ (dP − δ) as one bf16x2 multiply of the two bf16-rounded factors (fp32 product, RN to bf16)
+__device__ __forceinline__ uint32_t mul_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 constexpr int kFbThreads = 320;
 constexpr int kFbMath = 256;
 
@@ -83,7 +98,7 @@ __device__ __forceinline__ void store_row_bf16(uint32_t taddr, __nv_bfloat16* ds
 // the next tile while the math warps work on the current one; S(k+2) is issued after PV(k) in
 // program order, so the in-order tensor pipe never overwrites P(k) before it is consumed.
 // =====================================================================================
-template <int D, int E, bool TRAIN>
+template <int D, int E, bool TRAIN, bool CU>
 __global__ void __launch_bounds__(kFbThreads, 1)
 out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
            const __grid_constant__ CUtensorMap tv, Geom g, AlphaParams ap, const float* __restrict__ tau,
@@ -208,9 +223,13 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
           if (E != 1 && E != 2) xmax = fmaxf(xmax, fmaxf(x.x, x.y));
           float2 p, u;
           p_and_u2<E>(x, ap, p, u);
-          su = fadd2(su, u);
+          // U enters the U·V MMA rounded to bf16 (c14); with CU, ‖U‖₁ is summed from the same rounded
+          // values (reading r9)
+          const uint32_t ub = ptx::pack_bf16(u.x, u.y);
+          if constexpr (CU) su = fadd2(su, bf16x2_to_float2(ub));
+          else su = fadd2(su, u);
           pp[e >> 1] = ptx::pack_bf16(p.x, p.y);
-          pu[e >> 1] = ptx::pack_bf16(u.x, u.y);
+          pu[e >> 1] = ub;
         }
       };
       if (masked) body(std::true_type{}); else body(std::false_type{});
@@ -272,7 +291,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 // TMEM: S [0,128), dP [128,256), dS [256,320) (wg·32 + …), dQ [320, 320+D).
 // Issue order S,dP(k+1) | dQ(k): the next tile's scores are computed while the math warps form dS(k).
 // =====================================================================================
-template <int D, int E>
+template <int D, int E, bool CU>
 __global__ void __launch_bounds__(kFbThreads, 1)
 dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
           const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
@@ -396,8 +415,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
             }
             float2 p, u;
             p_and_u2<E>(x, ap, p, u);
-            const float2 ds = fmul2(u, fadd2(make_float2(dp[e], dp[e + 1]), ndl2));
-            pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+            const float2 g2 = fadd2(make_float2(dp[e], dp[e + 1]), ndl2);
+            if constexpr (CU)   // Û (r9)
+              pd[hh * 16 + (e >> 1)] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
+            else {
+              const float2 ds = fmul2(u, g2);
+              pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+            }
           }
         };
         if (masked) body(std::true_type{}); else body(std::false_type{});
@@ -429,7 +453,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
 //         next step's Sᵀ/dPᵀ overlap this step's math.
 // d = 128: Pᵀ/dSᵀ overwrite each warpgroup's own Sᵀ/dPᵀ columns (dV [256,384), dK [384,512)).
 // =====================================================================================
-template <int D, int E>
+template <int D, int E, bool CU>
 __global__ void __launch_bounds__(kFbThreads, 1)
 dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
             const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
@@ -577,9 +601,14 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
               }
               float2 p, u;
               p_and_u2<E>(x, ap, p, u);
-              const float2 ds = fmul2(u, fadd2(make_float2(dp[q4 * 4 + e], dp[q4 * 4 + e + 1]), dq2));
+              const float2 g2 = fadd2(make_float2(dp[q4 * 4 + e], dp[q4 * 4 + e + 1]), dq2);
               pp[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(p.x, p.y);
-              pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+              if constexpr (CU)   // Û (r9)
+                pd[hh * 16 + q4 * 2 + (e >> 1)] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
+              else {
+                const float2 ds = fmul2(u, g2);
+                pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+              }
             }
           }
         };
