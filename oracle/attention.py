@@ -44,10 +44,11 @@ def _row_chunks(rows, n_keys):
         yield rows[a:a + step]
 
 
-def solve_tau(q, k, alpha, causal, n_iter=None, scale=None, rows=None):
+def solve_tau(q, k, alpha, causal, n_iter=None, scale=None, rows=None, dtype=np.float64):
     """τ per query row: Alg. 1 mirror for ``n_iter`` iterations, or the exact
     threshold when ``n_iter`` is None.  Pre-scaled convention z = (α−1)·S (Alg. 1
-    line 3), i.e. the τ of Eq. 2."""
+    line 3), i.e. the τ of Eq. 2.  ``dtype``: precision of the mirror's iteration
+    (halley_bisection); the scores are float64 either way."""
     n, d = np.asarray(q).shape
     scale = default_scale(d) if scale is None else scale
     rows = np.arange(n) if rows is None else np.asarray(rows)
@@ -55,7 +56,8 @@ def solve_tau(q, k, alpha, causal, n_iter=None, scale=None, rows=None):
     pos = 0
     for rc in _row_chunks(rows, k.shape[0]):
         z = (alpha - 1.0) * scores(q, k, scale, causal, rc)
-        out[pos:pos + len(rc)] = tau_exact(z, alpha) if n_iter is None else halley_bisection(z, alpha, n_iter)
+        out[pos:pos + len(rc)] = (tau_exact(z, alpha) if n_iter is None
+                                  else halley_bisection(z, alpha, n_iter, dtype=dtype))
         pos += len(rc)
     return out
 

@@ -60,16 +60,26 @@ def halley_update(f, f1, f2, tau):
 
 
 def halley_bisection(z: np.ndarray, alpha: float, T: int, return_state: bool = False,
-                     halley: bool = True):
+                     halley: bool = True, dtype=np.float64):
     """Alg. 1 run for exactly T iterations, row-wise (the "T-step
     mirror" the GPU is compared against).  Each iteration: evaluate f, f', f'' at
     the current τ; bracket update (line 8); Halley candidate (line 9); accept it iff
     inside the *updated* bracket [τ_lo, τ_hi] (inclusive, line 10), else take the
     midpoint (line 13).  The returned τ is the one after the T-th update (reading
     c4).  ``halley=False`` gives the pure-bisection scheme of Eq. 4 whose answer is
-    the midpoint after the last bracket update."""
+    the midpoint after the last bracket update.
+
+    ``dtype=np.float32`` runs the same steps in float32 arithmetic: Alg. 1's discrete
+    decisions (the sign of f in Eq. 4, the Halley acceptance test) then fall where a float32
+    implementation's can, which a parity check needs when T is too small for the iteration to
+    have converged (a near-tie decided differently in float64 sends the float64 mirror down
+    another branch).  The float64 mirror is the reference; this is its float32-precision twin
+    (reading r10)."""
     if T < 1:
         raise ValueError("T >= 1 required (S:L54)")
+    if dtype is not np.float64:
+        with np.errstate(all="ignore"):
+            return _halley_bisection_lowp(np.asarray(z, dtype=dtype), alpha, T, halley, dtype)
     z = np.asarray(z, dtype=np.float64)
     tau_lo, tau_hi, tau = bracket_init(z, alpha)
     history = []
@@ -88,6 +98,36 @@ def halley_bisection(z: np.ndarray, alpha: float, T: int, return_state: bool = F
     if return_state:
         return tau, tau_lo, tau_hi, history
     return tau
+
+
+def _halley_bisection_lowp(z, alpha, T, halley, dt):
+    """Alg. 1 exactly as above, every operation in ``dt`` (see halley_bisection)."""
+    a = dt(alpha)
+    one, two, half = dt(1.0), dt(2.0), dt(0.5)
+    e = one / (a - one)
+    m = z.max(-1)
+    n = np.isfinite(z).sum(-1).astype(dt)
+    lo = m - one
+    hi = m - np.power(n, one - a)
+    tau = half * (lo + hi)
+    for _ in range(T):
+        x = z - tau[..., None]
+        pos = x > 0
+        xp = np.where(pos, x, dt(1.0))
+        f = np.where(pos, np.power(xp, e), dt(0)).sum(-1, dtype=dt) - one
+        f1 = -e * np.where(pos, np.power(xp, e - one), dt(0)).sum(-1, dtype=dt)
+        f2 = ((two - a) / ((a - one) * (a - one))) * np.where(pos, np.power(xp, e - two), dt(0)).sum(-1, dtype=dt)
+        neg = f < 0
+        lo, hi = np.where(neg, lo, tau), np.where(neg, tau, hi)
+        mid = half * (lo + hi)
+        if halley:
+            den = two * f1 * f1 - f * f2
+            th = tau - two * f * f1 / den
+            ok = np.isfinite(th) & (den != 0) & (th >= lo) & (th <= hi)
+            tau = np.where(ok, th, mid)
+        else:
+            tau = mid
+    return tau.astype(np.float64)
 
 
 # ---------------------------------------------------------------------------

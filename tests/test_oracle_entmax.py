@@ -220,3 +220,26 @@ def test_vjp_null_space_and_fd():
             sm_[:, j] -= h
             fd[:, j] = ((E.entmax(sp, alpha) - E.entmax(sm_, alpha)) * dp).sum(1) / (2 * h)
         np.testing.assert_allclose(g, fd, atol=1e-6)
+
+
+def test_float32_mirror_is_the_same_algorithm():
+    """The float32-precision twin of the Alg. 1 mirror (reading r10) follows the same steps: it
+    agrees with the float64 mirror to float32 rounding once the iteration has converged, keeps the
+    bracket invariants, and reproduces the SPEC worked examples."""
+    import synth
+    s, _ = synth.rowwise_scores(64, 2048, 5)
+    for alpha in (1.25, 1.5, 2.0, 1.7):
+        z = (alpha - 1.0) * s.astype(np.float64)
+        T = 6
+        t64 = E.halley_bisection(z, alpha, T)
+        t32 = E.halley_bisection(z, alpha, T, dtype=np.float32)
+        assert np.all(np.abs(t32 - t64) <= 4e-6 * np.maximum(1.0, np.abs(t64))), alpha
+        m = z.max(-1)
+        assert np.all(t32 >= m - 1.0 - 1e-6) and np.all(t32 <= m + 1e-6)
+    for zz, tau in (([0.5, 0.2], -0.15), ([0.0, 0.0], -0.5)):   # α = 2 (SPEC S:L85-87)
+        t = E.halley_bisection(np.array([zz]), 2.0, 8, dtype=np.float32)[0]
+        assert abs(t - tau) < 1e-6
+    # bisection-only mode: the same midpoint sequence
+    z = 0.5 * s[:8].astype(np.float64)
+    assert np.allclose(E.halley_bisection(z, 1.5, 10, halley=False),
+                       E.halley_bisection(z, 1.5, 10, halley=False, dtype=np.float32), atol=1e-5)
