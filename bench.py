@@ -95,7 +95,7 @@ class ClockSampler:
         "sw_power_cap": 0x0000000000000004,
     }
 
-    def __init__(self, device_index=0, period=0.01):
+    def __init__(self, device_index=0, period=0.002):
         self.samples, self.reasons, self.period = [], set(), period
         self.ok = False
         try:
