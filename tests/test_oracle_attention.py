@@ -192,3 +192,24 @@ def test_planted_generator_realises_target_density():
         for i in range(M.shape[0]):
             assert np.array_equal(np.nonzero(M[i])[0], owned[i])
         assert margin > 1e-2
+
+
+def test_parity_mirror_selection_prefers_the_matching_precision():
+    """tests/parity.mirror_tau (reading r10) returns the float64 mirror when the GPU τ agrees with
+    it, and, row by row, the float32 twin when the GPU τ sits on that twin's branch."""
+    from tests.parity import mirror_tau
+    import synth
+    found = False
+    for seed, N, alpha, T in ((13, 2, 1.5, 2), (20, 5, 1.5, 2), (23, 3, 2.0, 1)):   # known divergences
+        q, k, _, _ = synth.gaussian_head(N, 16, seed=seed)
+        q, k = q.astype(np.float64), k.astype(np.float64)
+        if True:
+            t64 = O.solve_tau(q, k, alpha, True, T)
+            t32 = O.solve_tau(q, k, alpha, True, T, dtype=np.float32)
+            assert np.array_equal(mirror_tau(q, k, alpha, True, T, t64.copy()), t64)
+            diff = np.abs(t32 - t64) > 1e-6
+            if diff.any():
+                got = mirror_tau(q, k, alpha, True, T, t32.copy())
+                assert np.array_equal(got[diff], t32[diff])
+                found = True
+    assert found, "no float32/float64 branch divergence found to exercise the selection"
