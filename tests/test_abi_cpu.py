@@ -133,3 +133,16 @@ def test_too_many_heads_rejected_before_launch():
     rc = L.entmax_attn_fwd(fake, fake, fake, ctypes.byref(s), 0, 1.5, 0, 3, 0.0,
                            fake, fake, fake, fake, fake, fake, fake, 1 << 40, None)
     assert rc == 2 and b"65535" in L.entmax_attn_last_error()
+
+
+def test_no_cpu_fallback():
+    """The product path never computes on the host: CPU tensors are rejected loudly."""
+    import torch
+    import paper_2502_12082_b200 as P
+    x = torch.zeros(1, 1, 128, 64, dtype=torch.bfloat16)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.entmax_attn_fwd(x, x, x, 1.5, False, 3)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.entmax_rowwise_fwd(torch.zeros(4, 64), 1.5, 3)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        P.entmax_attention(x, x, x)
