@@ -124,8 +124,8 @@ int col_lists_launch(const uint8_t* mask, const Geom& g, int32_t* col_cnt, int32
   const long long n = (long long)g.B * g.H * g.Tc;
   {
     ProfScope ps("col_lists", st);
-    launch_pdl(col_lists_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, mask, g.B * g.H, g.Tr, g.Tc,
-               col_cnt, col_idx);
+    launch_pdl(col_lists_kernel, dim3((unsigned)((n * 32 + 255) / 256)), dim3(256), 0, st, mask, g.B * g.H, g.Tr,
+               g.Tc, col_cnt, col_idx);   // one warp per (head, key block)
   }
   return cuda_status("col_lists");
 }

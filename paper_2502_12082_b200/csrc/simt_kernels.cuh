@@ -342,17 +342,25 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, co
 // 𝒦_j = {i | M_ij = 1} from the mask, increasing i; one thread per (head, j).
 __global__ void col_lists_kernel(const uint8_t* __restrict__ mask, int BH, int Tr, int Tc,
                                  int32_t* __restrict__ col_cnt, int32_t* __restrict__ col_idx) {
+  // one warp per (head, key block j): the lanes read 32 rows of the column at once and a ballot
+  // compacts them in increasing i (the thread-per-column loop was a chain of dependent loads)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");   // (launched with PDL: see runtime.h)
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)BH * Tc) return;
-  const int bh = (int)(t / Tc), j = (int)(t - (long long)(t / Tc) * Tc);
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (long long)BH * Tc) return;
+  const int bh = (int)(w / Tc), j = (int)(w - (long long)(w / Tc) * Tc);
   const uint8_t* m = mask + (long long)bh * Tr * Tc + j;
   int32_t* out = col_idx + ((long long)bh * Tc + j) * Tr;
   int cnt = 0;
-  for (int i = 0; i < Tr; ++i)
-    if (m[(long long)i * Tc]) out[cnt++] = i;
-  col_cnt[t] = cnt;
+  for (int i0 = 0; i0 < Tr; i0 += 32) {
+    const int i = i0 + lane;
+    const bool f = i < Tr && m[(long long)i * Tc] != 0;
+    const uint32_t b = __ballot_sync(0xffffffffu, f);
+    if (f) out[cnt + __popc(b & ((1u << lane) - 1u))] = i;
+    cnt += __popc(b);
+  }
+  if (lane == 0) col_cnt[w] = cnt;
 }
 
 // bit-packed mask: one thread per output word (32 mask bytes)
