@@ -148,9 +148,11 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const long long li = (long long)bh * g.Tr + i;
   // warm-up: the first W blocks only raise the running max and are streamed again at the end
 #ifndef ENTMAX_TAU_WDIV
-#define ENTMAX_TAU_WDIV 4   // (diagnostics builds vary it; 4 measured best of 2, 4, 8)
+// warm-up = nkb / WDIV tiles: measured best of {2, 3, 4, 8, 16}: 4 at d = 64, 3 at d = 128 (where the
+// MMA share of a tile is larger, so re-streaming is relatively cheaper than transient appends)
+#define ENTMAX_TAU_WDIV (D == 128 ? 3 : 4)
 #endif
-  const int W = nkb >= 32 ? max(4, nkb / ENTMAX_TAU_WDIV) : nkb / ENTMAX_TAU_WDIV;
+  const int W = nkb >= 32 ? max(4, nkb / (ENTMAX_TAU_WDIV)) : nkb / (ENTMAX_TAU_WDIV);
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_q, 1);
