@@ -542,7 +542,8 @@ def run_rowwise(P, synth, torch, dev, peaks, rows=8192, n=8192):
         out[dt_name] = {
             "halley_T3_ms": ms_h, "bisection_T23_ms": ms_b, "bwd_ms": ms_bwd,
             "roofline": {"kernel": "rowwise_fwd", "bound": "hbm", "achieved": ach, "peak": peaks["hbm"],
-                         "unit": "GB/s", "frac": ach / peaks["hbm"], "traffic": None,
+                         "unit": "GB/s", "frac": ach / peaks["hbm"],
+                         "traffic": ncu_traffic("rowwise_fwd") if dt_name == "f32" else None,
                          "algorithmic": f"{byt} B/launch (read s + write p + tau)"},
             "bwd_gbs": (rows * n * esz * 3) / (ms_bwd * 1e-3) / 1e9}
         del s, dp, p
