@@ -393,7 +393,7 @@ def main():
     mma_flops = {
         # one streaming pass of S = QKᵀ + the nkb/4 warm-up tiles it re-streams (the paper's Alg. 3 would
         # issue 1 + T passes; fallback tiers, taken by a few % of CTAs, are not counted)
-        "tau_sm100": 1.25 * 2.0 * d * vis_all,
+        "tau_sm100": (1.0 + (1 / 3 if d == 128 else 1 / 4)) * 2.0 * d * vis_all,   # warm-up nkb/4 (nkb/3 at d=128)
         "out_sm100": 6.0 * d * pairs,                             # S, P·V, U·V on candidate blocks
         "dkdv_sm100": 8.0 * d * pairs,                            # Sᵀ, dPᵀ, Pᵀ·dO, dSᵀ·Q
         "dq_sm100": 6.0 * d * pairs,                              # S, dP, dS·K
