@@ -25,8 +25,8 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``):
 No function is "parity unpinned".
 """
 from .rowwise import (relu_pow, root_f, bracket_init, bisection_update, halley_update,
-                     halley_bisection, tau_sparsemax, tau_entmax15, tau_bisect_exact,
+                     halley_bisection, halley_bisection_outcomes, tau_sparsemax, tau_entmax15, tau_bisect_exact,
                      tau_exact, entmax_probs, entmax, entmax_vjp)
-from .attention import (default_scale, scores, solve_tau, probs, u_of_p, attn_fwd,
+from .attention import (default_scale, scores, solve_tau, solve_tau_outcomes, probs, u_of_p, attn_fwd,
                         block_mask, mask_from_p, lookup_tables, attn_bwd,
-                        softmax_attention, fwd_bwd_heads)
+                        softmax_attention)

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .rowwise import entmax_probs, halley_bisection, tau_exact
+from .rowwise import entmax_probs, halley_bisection, halley_bisection_outcomes, tau_exact
 
 _CHUNK_ELEMS = 1 << 24
 
@@ -60,6 +60,29 @@ def solve_tau(q, k, alpha, causal, n_iter=None, scale=None, rows=None, dtype=np.
                                   else halley_bisection(z, alpha, n_iter, dtype=dtype))
         pos += len(rc)
     return out
+
+
+def solve_tau_outcomes(q, k, alpha, causal, n_iter, scale=None, rows=None):
+    """The T-step Alg. 1 mirror per query row plus its alternative valid outcomes through
+    near-ties (``halley_bisection_outcomes``, reading r10): returns (τ_T, alts) with alts of shape
+    (n_alt, len(rows)), NaN where a row has none."""
+    n, d = np.asarray(q).shape
+    scale = default_scale(d) if scale is None else scale
+    rows = np.arange(n) if rows is None else np.asarray(rows)
+    main = np.empty(len(rows))
+    alt_parts = []
+    pos = 0
+    for rc in _row_chunks(rows, k.shape[0]):
+        z = (alpha - 1.0) * scores(q, k, scale, causal, rc)
+        t, a = halley_bisection_outcomes(z, alpha, n_iter)
+        main[pos:pos + len(rc)] = t
+        alt_parts.append((pos, a))
+        pos += len(rc)
+    n_alt = max((a.shape[0] for _, a in alt_parts), default=0)
+    alts = np.full((n_alt, len(rows)), np.nan)
+    for p0, a in alt_parts:
+        alts[:a.shape[0], p0:p0 + a.shape[1]] = a
+    return main, alts
 
 
 def probs(q, k, tau_rows, alpha, causal, scale, rows):
@@ -195,27 +218,3 @@ def softmax_attention(q, k, v, causal=False, scale=None):
     s = s - s.max(1, keepdims=True)
     e = np.exp(s)
     return (e / e.sum(1, keepdims=True)) @ np.asarray(v, dtype=np.float64)
-
-
-def fwd_bwd_heads(q, k, v, dO, alpha, causal, n_iter, scale=None, Br=128, Bc=128):
-    """Batched convenience wrapper over heads: inputs [..., n, d]; loops heads."""
-    lead = q.shape[:-2]
-    qf = q.reshape((-1,) + q.shape[-2:])
-    out = {key: [] for key in ("tau", "O", "O2", "M", "dQ", "dK", "dV", "delta", "margin")}
-    for hh in range(qf.shape[0]):
-        qq, kk, vv = qf[hh], k.reshape(qf.shape)[hh], v.reshape(qf.shape)[hh]
-        fw = attn_fwd(qq, kk, vv, alpha, causal, n_iter, scale, Br, Bc)
-        M, margin = block_mask(qq, kk, fw["tau"], alpha, causal, scale, Br, Bc)
-        bw = attn_bwd(qq, kk, vv, dO.reshape(qf.shape)[hh], fw["tau"], alpha, causal, scale)
-        for key, val in (("tau", fw["tau"]), ("O", fw["O"]), ("O2", fw["O2"]), ("M", M),
-                         ("dQ", bw["dQ"]), ("dK", bw["dK"]), ("dV", bw["dV"]),
-                         ("delta", bw["delta"]), ("margin", margin)):
-            out[key].append(val)
-    res = {}
-    for key, vals in out.items():
-        if key == "margin":
-            res[key] = float(np.min(vals))
-        else:
-            arr = np.stack(vals)
-            res[key] = arr.reshape(lead + arr.shape[1:])
-    return res

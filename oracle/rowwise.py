@@ -60,7 +60,7 @@ def halley_update(f, f1, f2, tau):
 
 
 def halley_bisection(z: np.ndarray, alpha: float, T: int, return_state: bool = False,
-                     halley: bool = True, dtype=np.float64):
+                     halley: bool = True, dtype=np.float64, slack_ulps: int = 0):
     """Alg. 1 run for exactly T iterations, row-wise (the "T-step
     mirror" the GPU is compared against).  Each iteration: evaluate f, f', f'' at
     the current τ; bracket update (line 8); Halley candidate (line 9); accept it iff
@@ -74,12 +74,14 @@ def halley_bisection(z: np.ndarray, alpha: float, T: int, return_state: bool = F
     implementation's can, which a parity check needs when T is too small for the iteration to
     have converged (a near-tie decided differently in float64 sends the float64 mirror down
     another branch).  The float64 mirror is the reference; this is its float32-precision twin
-    (reading r10)."""
+    (reading r10).  ``slack_ulps`` (low precision only): accept a Halley candidate up to
+    that many ulps outside the bracket and clamp it in (reading r5, the GPU's finite-precision
+    form of line 10's inclusive test)."""
     if T < 1:
         raise ValueError("T >= 1 required (S:L54)")
     if dtype is not np.float64:
         with np.errstate(all="ignore"):
-            return _halley_bisection_lowp(np.asarray(z, dtype=dtype), alpha, T, halley, dtype)
+            return _halley_bisection_lowp(np.asarray(z, dtype=dtype), alpha, T, halley, dtype, slack_ulps)
     z = np.asarray(z, dtype=np.float64)
     tau_lo, tau_hi, tau = bracket_init(z, alpha)
     history = []
@@ -100,7 +102,89 @@ def halley_bisection(z: np.ndarray, alpha: float, T: int, return_state: bool = F
     return tau
 
 
-def _halley_bisection_lowp(z, alpha, T, halley, dt):
+def _alg1_step(z, alpha, tau, tau_lo, tau_hi, halley, flip_sign=None, flip_accept=None):
+    """One Alg. 1 iteration (lines 7-14) with optional forced flips of its two discrete decisions
+    (the Eq. 4 sign of f, the line-10 acceptance of the Halley candidate), rows where the flip mask
+    is True taking the other branch.  Returns (τ, τ_lo, τ_hi) and the decisions' relative margins."""
+    e = 1.0 / (alpha - 1.0)
+    f, f1, f2 = root_f(z, tau, alpha)
+    scale_t = np.maximum(1.0, np.abs(tau))
+    ssum = relu_pow(z - tau[..., None], e).sum(-1)
+    m_sign = np.abs(f) / (ssum + np.abs(f1) * scale_t)
+    if flip_sign is not None:
+        # the other side of a near-tie of Eq. 4: f of the opposite sign, same magnitude (a finite-
+        # precision run that sees the other sign computes its Halley candidate from that f too)
+        f = np.where(flip_sign, -f, f)
+    neg = f < 0
+    lo = np.where(neg, tau_lo, tau)
+    hi = np.where(neg, tau, tau_hi)
+    mid = 0.5 * (lo + hi)
+    if not halley:
+        return mid, lo, hi, m_sign, np.full_like(m_sign, np.inf)
+    tau_h, ok = halley_update(f, f1, f2, tau)
+    den = 2.0 * f1 * f1 - f * f2
+    with np.errstate(divide="ignore", invalid="ignore"):
+        m_den = np.where(ok, np.abs(den) / (2.0 * f1 * f1 + np.abs(f * f2)), np.inf)
+        th = np.where(ok, tau_h, 0.0)
+        # The updated bracket has τ itself at one end; the Halley step moves away from τ in the
+        # direction the sign of f gives (f >= 0 → τ = τ_lo and τ_H >= τ for den > 0), the same sign
+        # that moved the bracket, so a candidate is never in doubt at that end (a finite-precision
+        # run sees both with one sign) unless den is near 0.  The decision can only tie at the FAR
+        # end: relative distance of τ_H to it, inside or outside.
+        far = np.where(neg, lo, hi)
+        m_far = np.where(ok, np.abs(th - far) / scale_t, np.inf)
+    acc = ok & (th >= lo) & (th <= hi)
+    m_acc = np.minimum(m_far, m_den)
+    # A candidate ON the far end to within float64 rounding (Newton/Halley landing exactly on
+    # τ_lo = m − 1, e.g. a one-element support) is accepted by the inclusive test of exact
+    # arithmetic (reading c6) and by any finite-precision form of it with a rounding slack (r5):
+    # not a near-tie when accepted (a float64 rejection 1 ulp outside still is one).
+    m_acc = np.where(acc & (m_far <= 4.0 * np.finfo(np.float64).eps), m_den, m_acc)
+    if flip_accept is not None:
+        acc = np.where(flip_accept & ok, ~acc, acc)
+    return np.where(acc, th, mid), lo, hi, m_sign, m_acc
+
+
+def halley_bisection_outcomes(z: np.ndarray, alpha: float, T: int, halley: bool = True,
+                              margin: float = 3e-5, material: float = 1e-4):
+    """Alg. 1 for T iterations in float64, plus every *other* valid outcome a
+    finite-precision run could reach through a near-tie (reading r10).
+
+    Each iteration takes two discrete decisions: the sign of f(τ) in Eq. 4 and the
+    acceptance of the Halley candidate in line 10 (inside the updated bracket, finite, non-zero
+    denominator).  A float32 implementation rounds z, τ and the sums at ~1e-7 relative, so where a
+    decision's relative margin (``_alg1_step``) is below ``margin`` it may go the other way.  For
+    every such decision the run is forked with that one decision flipped and continued to T
+    iterations; forks whose final τ differs from the main run by more than ``material``·max(1, |τ|)
+    are alternative outcomes.  Returns (τ_T, alts) with alts of shape (n_alt, rows) (NaN where a
+    row has no material near-tie).  Decided from the float64 trajectory alone — never from a value
+    under test."""
+    z = np.asarray(z, dtype=np.float64)
+    lo, hi, tau = bracket_init(z, alpha)
+    states = []
+    for _ in range(T):
+        states.append((tau, lo, hi))
+        tau, lo, hi, _, _ = _alg1_step(z, alpha, tau, lo, hi, halley)
+    main = tau
+    alts = []
+    for t, (tau0, lo0, hi0) in enumerate(states):
+        _, _, _, m_sign, m_acc = _alg1_step(z, alpha, tau0, lo0, hi0, halley)
+        for kind, m in (("sign", m_sign), ("accept", m_acc)):
+            near = m < margin
+            if not near.any():
+                continue
+            fs = near if kind == "sign" else None
+            fa = near if kind == "accept" else None
+            tt, ll, hh, _, _ = _alg1_step(z, alpha, tau0, lo0, hi0, halley, flip_sign=fs, flip_accept=fa)
+            for _ in range(t + 1, T):
+                tt, ll, hh, _, _ = _alg1_step(z, alpha, tt, ll, hh, halley)
+            differs = near & (np.abs(tt - main) > material * np.maximum(1.0, np.abs(main)))
+            if differs.any():
+                alts.append(np.where(differs, tt, np.nan))
+    return main, (np.stack(alts) if alts else np.empty((0,) + main.shape))
+
+
+def _halley_bisection_lowp(z, alpha, T, halley, dt, slack_ulps=0):
     """Alg. 1 exactly as above, every operation in ``dt`` (see halley_bisection)."""
     a = dt(alpha)
     one, two, half = dt(1.0), dt(2.0), dt(0.5)
@@ -123,8 +207,9 @@ def _halley_bisection_lowp(z, alpha, T, halley, dt):
         if halley:
             den = two * f1 * f1 - f * f2
             th = tau - two * f * f1 / den
-            ok = np.isfinite(th) & (den != 0) & (th >= lo) & (th <= hi)
-            tau = np.where(ok, th, mid)
+            sl = dt(slack_ulps) * np.finfo(dt).eps * np.maximum(np.abs(lo), np.abs(hi))
+            ok = np.isfinite(th) & (den != 0) & (th >= lo - sl) & (th <= hi + sl)
+            tau = np.where(ok, np.minimum(np.maximum(th, lo), hi), mid)
         else:
             tau = mid
     return tau.astype(np.float64)

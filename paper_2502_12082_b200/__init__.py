@@ -91,6 +91,34 @@ class FwdResult:
     row_idx: torch.Tensor  # [B,H,T_r,T_c] int32
 
 
+def _check_fwd_result(r: FwdResult, q: torch.Tensor, training: bool, masked: bool, need_o: bool = True):
+    """Shapes, dtypes, layouts and device of a FwdResult against q (the kernels index τ by
+    bh·N + row and the tables by B·H·T_r·T_c: a mismatch would read or write out of bounds)."""
+    B, H, N, d = q.shape
+    br, bc = block_size()
+    Tr, Tc = -(-N // br), -(-N // bc)
+
+    def chk(t, shape, dtype, name, contiguous=True):
+        if t is None:
+            raise ValueError(f"{name} is missing")
+        if tuple(t.shape) != shape or t.dtype != dtype or t.device != q.device or (contiguous and not t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {shape} on {q.device}")
+
+    if need_o:
+        if r.o is None or r.o.shape != q.shape or r.o.stride() != q.stride() or r.o.dtype != q.dtype \
+                or r.o.device != q.device:
+            raise ValueError("o must share q's shape, strides, dtype and device")
+    if training:
+        chk(r.o2, (B, H, N, d), torch.float32, "o2")
+    chk(r.tau, (B, H, N), torch.float32, "tau")
+    if masked:
+        chk(r.mask, (B, H, Tr, Tc), torch.uint8, "mask")
+        chk(r.row_cnt, (B, H, Tr), torch.int32, "row_cnt")
+        chk(r.row_idx, (B, H, Tr, Tc), torch.int32, "row_idx")
+    elif any(t is not None for t in (r.mask, r.row_cnt, r.row_idx)):
+        raise ValueError("unmasked mode: mask, row_cnt and row_idx must all be None")
+
+
 def entmax_attn_fwd(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, training=True,
                     out: FwdResult | None = None, workspace: torch.Tensor | None = None,
                     masked: bool = True) -> FwdResult:
@@ -105,12 +133,15 @@ def entmax_attn_fwd(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, trai
     dev = q.device
     if out is None:
         out = FwdResult(
-            o=torch.empty_like(q),
+            # O is written with q's strides (the ABI's "same strides" contract): allocate it so
+            o=torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=dev),
             o2=torch.empty(q.shape, dtype=torch.float32, device=dev) if training else None,
             tau=torch.empty((B, H, N), dtype=torch.float32, device=dev),
             mask=torch.empty((B, H, Tr, Tc), dtype=torch.uint8, device=dev) if masked else None,
             row_cnt=torch.empty((B, H, Tr), dtype=torch.int32, device=dev) if masked else None,
             row_idx=torch.empty((B, H, Tr, Tc), dtype=torch.int32, device=dev) if masked else None)
+    else:
+        _check_fwd_result(out, q, training, masked)
     ws_bytes = L.entmax_attn_fwd_workspace_bytes(ctypes.byref(s), _DT[q.dtype], int(causal))
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
@@ -127,13 +158,18 @@ def entmax_attn_bwd(q, k, v, d_o, fwd: FwdResult, alpha=1.5, causal=False, scale
     """Backward pass through the C ABI; returns (dq, dk, dv)."""
     if fwd.o2 is None:
         raise ValueError("backward needs O⁽²⁾: run the forward with training=True")
-    d_o = d_o.contiguous() if d_o.stride() != q.stride() else d_o
+    if d_o.stride() != q.stride() and d_o.shape == q.shape:   # the ABI reads dO with q's strides
+        d_o = torch.empty_strided(q.shape, q.stride(), dtype=d_o.dtype, device=d_o.device).copy_(d_o)
     _check_inputs(q, k, v, d_o)
-    if fwd.o2.dtype != torch.float32 or not fwd.o2.is_contiguous() or fwd.o2.shape != q.shape:
-        raise ValueError("o2 must be the fp32 contiguous [B,H,N,d] tensor written by entmax_attn_fwd")
+    _check_fwd_result(fwd, q, True, fwd.mask is not None, need_o=False)
     L = _lib.lib()
     s = _shape(q)
-    dq, dk, dv = grads if grads is not None else (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
+    if grads is None:   # written with q's strides (ABI contract), whatever the inputs' layout
+        grads = tuple(torch.empty_strided(q.shape, q.stride(), dtype=q.dtype, device=q.device) for _ in range(3))
+    for g in grads:
+        if g.shape != q.shape or g.stride() != q.stride() or g.dtype != q.dtype or g.device != q.device:
+            raise ValueError("grads must share q's shape, strides, dtype and device")
+    dq, dk, dv = grads
     ws_bytes = L.entmax_attn_bwd_workspace_bytes(ctypes.byref(s), _DT[q.dtype], int(causal))
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)

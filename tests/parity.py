@@ -37,17 +37,32 @@ def rel_l2(a, b, floor_rms=1e-4):
     return float(np.linalg.norm(a - b) / den)
 
 
-def mirror_tau(q, k, alpha, causal, n_iter, tau_gpu, rows=None):
-    """Reference τ: the T-step Alg. 1 mirror in float64 — or, row by row, its float32-precision
-    twin where the GPU's τ lies closer to that one (DESIGN.md r10: with T too small to have
-    converged, a near-tie in Eq. 4 / the Halley test can be decided differently at float32 and
-    float64 precision, and both are faithful runs of Alg. 1).  The chosen τ then defines every
-    reference output, so O, the mask and the gradients are still checked against it exactly."""
-    t64 = O.solve_tau(q, k, alpha, causal, n_iter, rows=rows)
-    if np.allclose(tau_gpu, t64, rtol=0, atol=1e-6):
+# fraction of query rows allowed to carry near-tie alternatives (reading r10): a converged run
+# (T >= 3, the paper's setting) has almost none; with T < 3 the unconverged iteration is close to a
+# decision on more rows
+MAX_FLAGGED = {True: 0.02, False: 0.35}
+
+
+def mirror_tau(q, k, alpha, causal, n_iter, tau_gpu, rows=None, report=None):
+    """Reference τ: the T-step Alg. 1 mirror in float64.  Where the ORACLE finds that a discrete
+    decision of the run (the sign of f in Eq. 4, the Halley acceptance of line 10) fell within
+    float32 resolution of a tie AND the other branch leads to a materially different τ_T
+    (``oracle.halley_bisection_outcomes``, decided from the float64 trajectory alone), the row has
+    several valid results; only for those rows the reference is the valid outcome the GPU's τ
+    matches (DESIGN.md r10).  Every other row is held to the float64 mirror.  The flagged fraction
+    is bounded (MAX_FLAGGED) and reported.  The chosen τ then defines every reference output."""
+    t64, alts = O.solve_tau_outcomes(q, k, alpha, causal, n_iter, rows=rows)
+    flagged = np.isfinite(alts).any(0) if alts.size else np.zeros(t64.shape, bool)
+    frac = float(flagged.mean()) if flagged.size else 0.0
+    assert frac <= MAX_FLAGGED[n_iter >= 3], ("too many near-tie rows", frac, n_iter)
+    if report is not None:
+        report.append(dict(near_tie_rows=int(flagged.sum()), rows=int(flagged.size)))
+    if not flagged.any():
         return t64
-    t32 = O.solve_tau(q, k, alpha, causal, n_iter, rows=rows, dtype=np.float32)
-    return np.where(np.abs(tau_gpu - t32) < np.abs(tau_gpu - t64), t32, t64)
+    cand = np.concatenate([t64[None], alts], 0)
+    dist = np.where(np.isfinite(cand), np.abs(cand - tau_gpu[None]), np.inf)
+    best = cand[np.argmin(dist, 0), np.arange(t64.size)]
+    return np.where(flagged, best, t64)
 
 
 def check_head(res, ref_inputs, bh, alpha, causal, n_iter, dtype, with_bwd=True, grads=None, report=None):
@@ -56,7 +71,8 @@ def check_head(res, ref_inputs, bh, alpha, causal, n_iter, dtype, with_bwd=True,
     N = q.shape[0]
     tol = TOL[dtype]
     tau_g = res.tau.reshape(-1, N)[bh].double().cpu().numpy()
-    fw = O.attn_fwd(q, k, v, alpha, causal, n_iter, tau=mirror_tau(q, k, alpha, causal, n_iter, tau_g))
+    nt = []
+    fw = O.attn_fwd(q, k, v, alpha, causal, n_iter, tau=mirror_tau(q, k, alpha, causal, n_iter, tau_g, report=nt))
     err_tau = np.max(np.abs(tau_g - fw["tau"]) / np.maximum(1.0, np.abs(fw["tau"])))
     assert err_tau <= TAU_RTOL, ("tau", bh, err_tau)
     d = q.shape[1]
@@ -77,7 +93,7 @@ def check_head(res, ref_inputs, bh, alpha, causal, n_iter, dtype, with_bwd=True,
     idx = res.row_idx.reshape(-1, Tr, Tc)[bh].cpu().numpy()
     for i in range(Tr):
         assert cnt[i] == len(Qt[i]) and np.array_equal(idx[i, :cnt[i]], Qt[i]), ("row table", bh, i)
-    out = dict(tau=err_tau, O=err_o, margin=margin, density=float(M_ref.mean()))
+    out = dict(tau=err_tau, O=err_o, margin=margin, density=float(M_ref.mean()), **nt[0])
     if with_bwd and grads is not None:
         bw = O.attn_bwd(q, k, v, do, fw["tau"], alpha, causal)
         for name, g_gpu, g_ref in zip(("dQ", "dK", "dV"), grads, (bw["dQ"], bw["dK"], bw["dV"])):

@@ -32,6 +32,8 @@ CASES = [
     (1, 2, 384, 128, torch.bfloat16, 1.5, True, 3),     # d = 128
     (1, 1, 640, 128, torch.bfloat16, 1.75, False, 4),   # generic α (non-integer exponent)
     (1, 1, 200, 32, torch.float32, 1.5, True, 3),       # SIMT-only head dim
+    (1, 1, 256, 64, torch.float32, 2.0, False, 5),      # fp32 bar at α = 2 (sparsemax; O2 reading r11)
+    (1, 2, 300, 64, torch.float32, 1.33, True, 4),      # fp32 bar at a generic α (non-integer 1/(α−1))
 ]
 
 
@@ -127,10 +129,12 @@ def test_parity_transient_overflow_rebuild(N, causal):
         check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
 
 
-@pytest.mark.parametrize("alpha,causal,d", [(1.1, False, 64), (1.33, True, 64), (1.9, False, 64), (1.6, True, 128)])
+@pytest.mark.parametrize("alpha,causal,d", [(1.1, False, 64), (1.33, True, 64), (1.9, False, 64), (1.6, True, 128),
+                                             (1.01, False, 64), (1.01, True, 128)])
 def test_parity_generic_alpha(alpha, causal, d):
     """Non-integer 1/(α−1): P, U via lg2/ex2 in the tcgen05 kernels, the τ sums
-    via the generic accumulation.  α = 1.1 gives e = 10 (steep powers), α = 1.9 e ≈ 1.11."""
+    via the generic accumulation.  α = 1.1 gives e = 10 (steep powers), α = 1.9 e ≈ 1.11; α = 1.01
+    (e = 100) is the start of the paper's α annealing."""
     _require_gpu()
     dev, ref = make_case(1, 2, 640, d, torch.bfloat16, seed=int(alpha * 100) + d)
     fw, grads = run_gpu(dev, alpha, causal, 4)
@@ -253,3 +257,28 @@ def test_pack_mask_bits():
                 col = 32 * w + b
                 want = mm[..., col] if col < Tc else np.zeros(mm.shape[:-1], np.uint8)
                 assert np.array_equal((pk[..., w] >> b) & 1, want.astype(np.uint32))
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_padded_layout_qkv_split(causal):
+    """q, k, v as views of one [B, H, N, 3d] buffer (row stride 3d, the fused-QKV layout the ABI's
+    strides allow): outputs and gradients are written with q's strides, stay inside their own
+    allocations, and match the oracle like contiguous inputs do."""
+    _require_gpu()
+    import paper_2502_12082_b200 as P
+    B, H, N, d = 1, 2, 384, 64
+    dev, ref = make_case(B, H, N, d, torch.bfloat16, seed=77)
+    qkv = torch.empty((B, H, N, 3 * d), dtype=torch.bfloat16, device="cuda")
+    for c in range(3):
+        qkv[..., c * d:(c + 1) * d] = dev[c]
+    q, k, v = qkv[..., :d], qkv[..., d:2 * d], qkv[..., 2 * d:]
+    guard = qkv.clone()
+    fw = P.entmax_attn_fwd(q, k, v, 1.5, causal, 3)
+    grads = P.entmax_attn_bwd(q, k, v, dev[3], fw, 1.5, causal)
+    torch.cuda.synchronize()
+    assert fw.o.stride() == q.stride() and all(g.stride() == q.stride() for g in grads)
+    assert torch.equal(qkv, guard)                          # inputs untouched
+    for bh in range(B * H):
+        check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
+    fc, gc = run_gpu(dev, 1.5, causal, 3)                   # same bits as the contiguous layout
+    assert torch.equal(fc.o, fw.o) and all(torch.equal(a, b) for a, b in zip(gc, grads))

@@ -194,22 +194,89 @@ def test_planted_generator_realises_target_density():
         assert margin > 1e-2
 
 
-def test_parity_mirror_selection_prefers_the_matching_precision():
-    """tests/parity.mirror_tau (reading r10) returns the float64 mirror when the GPU τ agrees with
-    it, and, row by row, the float32 twin when the GPU τ sits on that twin's branch."""
-    from tests.parity import mirror_tau
+def test_near_tie_outcomes_cover_every_float32_divergence():
+    """Reading r10: the oracle's near-tie fork (halley_bisection_outcomes) must contain every
+    result a float32 run of Alg. 1 (with the r5 slack) reaches when it branches away from the
+    float64 mirror.  Swept over small causal heads at T = 1..3 where divergences occur; the main
+    run is bitwise the mirror."""
     import synth
-    found = False
-    for seed, N, alpha, T in ((13, 2, 1.5, 2), (20, 5, 1.5, 2), (23, 3, 2.0, 1)):   # known divergences
-        q, k, _, _ = synth.gaussian_head(N, 16, seed=seed)
-        q, k = q.astype(np.float64), k.astype(np.float64)
-        if True:
-            t64 = O.solve_tau(q, k, alpha, True, T)
-            t32 = O.solve_tau(q, k, alpha, True, T, dtype=np.float32)
-            assert np.array_equal(mirror_tau(q, k, alpha, True, T, t64.copy()), t64)
-            diff = np.abs(t32 - t64) > 1e-6
-            if diff.any():
-                got = mirror_tau(q, k, alpha, True, T, t32.copy())
-                assert np.array_equal(got[diff], t32[diff])
-                found = True
-    assert found, "no float32/float64 branch divergence found to exercise the selection"
+    div = 0
+    for seed in range(60):
+        for N in (2, 3, 5, 9, 17, 40):
+            for alpha in (1.25, 1.5, 2.0, 1.33):
+                for T in (1, 2, 3):
+                    q, k, _, _ = synth.gaussian_head(N, 16, seed=seed)
+                    z = (alpha - 1) * O.scores(q.astype(np.float64), k.astype(np.float64), 0.25, True)
+                    t64, alts = O.halley_bisection_outcomes(z, alpha, T)
+                    assert np.array_equal(t64, O.halley_bisection(z, alpha, T))
+                    t32 = O.halley_bisection(z, alpha, T, dtype=np.float32, slack_ulps=8)
+                    d = np.abs(t32 - t64) > 1e-3 * np.maximum(1.0, np.abs(t64))
+                    if d.any():
+                        div += int(d.sum())
+                        assert alts.size, (seed, N, alpha, T)
+                        near = np.abs(alts[:, d] - t32[d]) <= 1e-3 * np.maximum(1.0, np.abs(t32[d]))
+                        assert near.any(0).all(), (seed, N, alpha, T)
+    assert div >= 5, "no float32/float64 branch divergence found to exercise the fork"
+
+
+def test_near_tie_fork_flags_an_exact_tie_and_spares_converged_rows():
+    """A row whose Eq. 4 decision is an exact tie gets an alternative outcome; rows of the paper's
+    Gaussian benchmark at T >= 3 (converged) get almost none; mirror_tau holds every unflagged row
+    to the float64 mirror whatever value the GPU reports."""
+    from tests.parity import mirror_tau
+    # α = 2, z = [0, −1/2] (n = 2): bracket [−1, −1/2], τ0 = −3/4, f(τ0) = 3/4 + 1/4 − 1 = 0 exactly —
+    # an exact tie of Eq. 4 at the root: both branches give τ = −3/4 (immaterial), no alternative
+    z = np.array([[0.0, -0.5]])
+    lo, hi, tau0 = O.bracket_init(z, 2.0)
+    assert tau0[0] == -0.75 and O.root_f(z, tau0, 2.0)[0][0] == 0.0
+    t, alts = O.halley_bisection_outcomes(z, 2.0, 1)
+    assert t[0] == -0.75 and (alts.size == 0 or not np.isfinite(alts).any())
+    # Gaussian benchmark rows, T = 3: few flagged rows
+    import synth
+    q, k, _, _ = synth.gaussian_head(512, 64, seed=3)
+    q, k = q.astype(np.float64), k.astype(np.float64)
+    for alpha in (1.25, 1.5):
+        t64, alts = O.solve_tau_outcomes(q, k, alpha, False, 3)
+        flagged = np.isfinite(alts).any(0) if alts.size else np.zeros(512, bool)
+        assert flagged.mean() <= 0.02, (alpha, flagged.mean())
+        junk = t64 + 0.37                                   # a wrong "GPU" τ
+        got = mirror_tau(q, k, alpha, False, 3, junk)
+        assert np.array_equal(got[~flagged], t64[~flagged])
+
+
+@pytest.mark.parametrize("alpha", [1.25, 1.5, 2.0, 1.7])
+@pytest.mark.parametrize("causal", [False, True])
+def test_o2_matches_the_delta_identity(alpha, causal):
+    """P:L786-796 (Eq. getting_di): δ_i = U_iᵀ dP_i / ‖U_i‖₁ = dO_iᵀ O⁽²⁾_i.  attn_fwd's O⁽²⁾ must give
+    the δ of the first line computed densely (U = P^{2−α}, dP = dO Vᵀ), and the δ attn_bwd uses —
+    which the finite-difference gradient tests pin (dropping it breaks them)."""
+    rng = np.random.default_rng(31)
+    q, k, v = _qkv(96, 16, 30)
+    dO = rng.standard_normal(v.shape)
+    fw = O.attn_fwd(q, k, v, alpha, causal, exact=True)
+    delta_o2 = np.sum(dO * fw["O2"], 1)
+    p = O.probs(q, k, fw["tau"], alpha, causal, O.default_scale(16), np.arange(96))
+    u = np.where(p > 0, np.power(np.where(p > 0, p, 1.0), 2.0 - alpha), 0.0)
+    dP = dO @ v.T
+    delta_first = (u * dP).sum(1) / u.sum(1)
+    np.testing.assert_allclose(delta_o2, delta_first, atol=1e-10, rtol=0)
+    bw = O.attn_bwd(q, k, v, dO, fw["tau"], alpha, causal)
+    np.testing.assert_allclose(delta_o2, bw["delta"], atol=1e-10, rtol=0)
+    assert np.abs(u.sum(1) - 1.0).max() > 1e-2 or alpha == 2.0   # ‖U‖₁ ≠ 1: normalisation matters
+
+
+def test_o2_hand_example_three_keys():
+    """One query, three keys, α = 1.5, c = 1, V = I.  Scaled scores z = (α−1)s = [0.5, 0, −2].
+    On the support {1, 2}: a = z1 − τ, b = a − 1/2, a² + b² = 1 (Eq. 3, e = 2) ⇒ 2a² − a − 3/4 = 0,
+    a = (1 + √7)/4, b = (√7 − 1)/4, τ = 1/2 − a; z3 − τ = −2 − τ < 0 (off the support).
+    P = [a², b², 0] (Eq. 2); U = P^{1/2} = [a, b, 0], ‖U‖₁ = √7/2 ≠ 1 (P:L793):
+    O = P, O⁽²⁾ = [a, b, 0]/(√7/2)."""
+    a = (1 + np.sqrt(7)) / 4
+    b = (np.sqrt(7) - 1) / 4
+    q = np.array([[1.0]])
+    k = np.array([[1.0], [0.0], [-4.0]])
+    fw = O.attn_fwd(q, k, np.eye(3), 1.5, False, exact=True, scale=1.0)
+    np.testing.assert_allclose(fw["tau"], [0.5 - a], atol=1e-14)
+    np.testing.assert_allclose(fw["O"][0], [a * a, b * b, 0.0], atol=1e-14)
+    np.testing.assert_allclose(fw["O2"][0], [a / (np.sqrt(7) / 2), b / (np.sqrt(7) / 2), 0.0], atol=1e-14)
+    np.testing.assert_allclose(fw["usum"], [np.sqrt(7) / 2], atol=1e-14)

@@ -243,3 +243,52 @@ def test_float32_mirror_is_the_same_algorithm():
     z = 0.5 * s[:8].astype(np.float64)
     assert np.allclose(E.halley_bisection(z, 1.5, 10, halley=False),
                        E.halley_bisection(z, 1.5, 10, halley=False, dtype=np.float32), atol=1e-5)
+
+
+@pytest.mark.parametrize("alpha", [1.25, 1.5, 1.7, 1.33, 2.0])
+def test_root_f_derivatives_by_central_differences(alpha):
+    """Eqs. 6-7: f′ and f″ returned by root_f are the derivatives of Eq. 3's f in τ.
+    Central differences of f (for f′) and of f′ (for f″) at τ values whose x = z − τ keep a distance
+    of at least 1e-3 from 0 (f is smooth there), for integer and non-integer 1/(α−1).  A dropped or
+    mis-scaled coefficient of Eq. 6 or 7 (e.g. (2−α)/(α−1) instead of (2−α)/(α−1)²) fails."""
+    rng = np.random.default_rng(17)
+    z = (alpha - 1.0) * rng.standard_normal((200, 64)) * 2
+    m = z.max(1)
+    tau = m - rng.uniform(0.05, 1.0, 200)
+    x = z - tau[:, None]
+    keep = np.min(np.abs(x), 1) > 1e-3
+    z, tau = z[keep], tau[keep]
+    assert len(tau) > 100
+    h = 1e-6
+    f, f1, f2 = E.root_f(z, tau, alpha)
+    fp, f1p, _ = E.root_f(z, tau + h, alpha)
+    fm, f1m, _ = E.root_f(z, tau - h, alpha)
+    np.testing.assert_allclose(f1, (fp - fm) / (2 * h), rtol=1e-6, atol=1e-7)
+    np.testing.assert_allclose(f2, (f1p - f1m) / (2 * h), rtol=1e-5, atol=1e-6)
+    if alpha != 2.0:
+        assert np.abs(f2).max() > 1e-2                      # the check is not vacuous
+
+
+def test_halley_convergence_alpha_125_p250_protocol():
+    """P:L246-250 protocol (n = 8192 N(0,1) rows) at α = 1.25 (e = 4): Halley-bisection converges
+    in a few iterations (cubic near the root: each iteration at least squares the error once in the
+    basin), far faster than bisection; with f″ replaced by 0 (a Newton-bisection, i.e. a wrong Eq. 7)
+    it is measurably slower — so the convergence claim depends on the f″ the oracle computes."""
+    rng = np.random.default_rng(2)
+    z = 0.25 * rng.standard_normal((32, 8192))
+    t_star = E.tau_bisect_exact(z, 1.25)
+    p_star = E.entmax_probs(z, t_star, 1.25)
+    errs = [np.abs(E.entmax_probs(z, E.halley_bisection(z, 1.25, T), 1.25) - p_star).mean() for T in range(1, 6)]
+    assert errs[2] <= 1e-8 and errs[4] <= 1e-15, errs
+    bis = np.abs(E.entmax_probs(z, E.halley_bisection(z, 1.25, 3, halley=False), 1.25) - p_star).mean()
+    assert bis > 1e3 * errs[2]
+    # Newton variant: same Alg. 1 loop with f″ := 0
+    lo, hi, tau = E.bracket_init(z, 1.25)
+    for _ in range(3):
+        f, f1, _ = E.root_f(z, tau, 1.25)
+        lo, hi = E.bisection_update(f, tau, lo, hi)
+        th, ok = E.halley_update(f, f1, np.zeros_like(f), tau)
+        ok &= (th >= lo) & (th <= hi)
+        tau = np.where(ok, th, 0.5 * (lo + hi))
+    newton = np.abs(E.entmax_probs(z, tau, 1.25) - p_star).mean()
+    assert newton > 10 * errs[2], (newton, errs[2])
