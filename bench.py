@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """bench.py — α-entmax attention fwd+bwd (AdaSplash hot path) on B200.
 
-Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]``;
-N > 1 is launched under torch.distributed.run (one rank per GPU, NCCL).  Rank 0 prints ONE
-JSON line.
+Contract (driver): ``python bench.py --gpus N --steps K --warmup W [--impl reference]``; N > 1
+runs one rank per GPU under torch.distributed.run (the driver launches it so; without an outer
+launcher bench.py re-executes itself under it).  Rank 0 prints ONE JSON line.
 
 Workload (BASELINE.json configs[1], the config the metric is quoted on):
-  B=4 H=12 N=8192 d=64 α=1.5 non-causal bf16, n_iter = 3, Gaussian inputs with
-  query variance σ² = 6 (the paper's benchmark generator) — per rank.  Weak scaling:
-  every rank runs its own B·H heads (distinct seeds per rank), no collective on the data path.
-One step = entmax_attn_fwd (τ + output + tables) + entmax_attn_bwd (δ, 𝒦 tables, dK/dV, dQ)
-over the whole batch.  value = effective TFLOP/s over all ranks, FA convention
-14·d·ΣV per fwd+bwd with V = visible (query, key) pairs of the non-skipped blocks
-(SURVEY §8d).  Inputs (201 MB per rank) exceed the 126 MB L2, so no explicit flush.
-``--sweep`` adds the planted-block-sparsity sweep (Fig. 1 analogue) as extra keys.
+  B=4 H=12 N=8192 d=64 α=1.5 non-causal bf16, n_iter = 3, Gaussian inputs with query variance
+  σ² = 6 (the paper's benchmark generator).  N > 1: the 48 heads are split over the ranks
+  (contiguous B·H/G heads per rank; "scaling": "strong"), each rank regenerating its
+  heads from per-head seeds; no collective on the data path; per-rank times and the max/mean
+  imbalance are reported, the weak split (every rank its own 48 heads) as an extra key.
+One step = entmax_attn_fwd (τ + output + tables) + entmax_attn_bwd (δ, 𝒦 tables, dK/dV, dQ) over
+the rank's heads.  value = effective TFLOP/s over all ranks, FA convention 14·d·ΣV per fwd+bwd
+with V = visible (query, key) pairs of the non-skipped blocks, ÷ the max-over-ranks
+time.  Inputs (201 MB at N = 1) exceed the 126 MB L2, so no explicit flush.
+Extra keys (rank 0, after the headline; --no-extras skips them): the planted block-sparsity sweep
+(Fig. 1 analogue, incl. a 99.2 %-sparse N = 16384 point), configs 3-5 (+ planted ρ = 0.05
+variants) beside same-box SDPA, the Fig. 3 sequence-length sweep (non-causal d = 64, N = 1k..64k),
+the standalone row-wise solver (NEXT-1) and a GPT-2-124M training step (NEXT-4).
 
 The oracle (test infrastructure, oracle/) is executed only for the ``cpu_baseline`` leg and
 for ``--impl reference``.
@@ -45,12 +50,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--sweep", action="store_true", default=True,
-                    help="add the planted block-sparsity sweep (default on; --no-sweep to skip)")
-    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
-    ap.add_argument("--suite", action="store_true", help="add configs 3-5 (seq-len / alpha / long-context lines)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = the B·H heads split over the ranks (SURVEY §8e, default); "
+                         "weak = every rank its own B·H heads")
+    ap.add_argument("--no-weak", action="store_true", help="N > 1 strong: skip the extra weak-scaling key")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false", help="skip the block-sparsity sweep")
+    ap.add_argument("--no-suite", dest="suite", action="store_false", help="skip the configs 3-5 lines")
+    ap.add_argument("--no-fig3", dest="fig3", action="store_false", help="skip the seq-len sweep (Fig. 3)")
+    ap.add_argument("--no-gpt2", dest="gpt2", action="store_false", help="skip the GPT-2 step line (NEXT-4)")
     ap.add_argument("--no-rowwise", action="store_true", help="skip the standalone row-wise solver line")
-    ap.add_argument("--gpt2", action="store_true", help="add the GPT-2-124M training-step line (NEXT-4)")
+    ap.add_argument("--no-extras", action="store_true", help="headline line only (no sweep/suite/fig3/...)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--N", type=int, default=CFG["N"])
     ap.add_argument("--d", type=int, default=CFG["d"])
@@ -221,47 +230,94 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------------------ native arm
-def main():
-    args = parse()
-    cfg = dict(B=args.B, H=args.H, N=args.N, d=args.d, alpha=args.alpha, causal=args.causal,
-               n_iter=args.n_iter, gen=args.gen, rho=args.rho)
-    if args.impl == "reference":
-        return run_reference(args, cfg)
+def maybe_reexec_under_torchrun(args):
+    """`bench.py --gpus N` (N > 1) without an outer launcher: re-exec under torch.distributed.run,
+    one rank per GPU on this node (the driver's own launch sets WORLD_SIZE and skips this)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
-    import torch
-    import torch.distributed as dist
-    import paper_2502_12082_b200 as P
-    import synth
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        world = max(world, 1)
-    # ENTMAX_BENCH_SHARE_GPU=1 / ENTMAX_BENCH_BACKEND=gloo: test hook to exercise the multi-rank path
-    # on a one-GPU box (ranks share cuda:0, gloo carries the barriers and the max-over-ranks timing)
-    if os.environ.get("ENTMAX_BENCH_SHARE_GPU") == "1":
-        local = local % torch.cuda.device_count()
-    backend = os.environ.get("ENTMAX_BENCH_BACKEND", "nccl")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+class Ranks:
+    """One process per GPU (torch.distributed, NCCL on the GPUs; gloo under the share-GPU test hook).
+    Every collective here is host plumbing for timing and checking — none is on the data path."""
 
-    B, H, N, d = cfg["B"], cfg["H"], cfg["N"], cfg["d"]
+    def __init__(self, torch, dist):
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        # ENTMAX_BENCH_SHARE_GPU=1 / ENTMAX_BENCH_BACKEND=gloo: test hook to exercise the multi-rank path
+        # on a one-GPU box (ranks share cuda:0, gloo carries the barriers and reductions)
+        if os.environ.get("ENTMAX_BENCH_SHARE_GPU") == "1":
+            local = local % torch.cuda.device_count()
+        elif self.world > torch.cuda.device_count():
+            raise SystemExit(f"bench: {self.world} ranks but only {torch.cuda.device_count()} visible GPUs")
+        self.backend = os.environ.get("ENTMAX_BENCH_BACKEND", "nccl")
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        self.local = local
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group(self.backend)
+
+    def _cdev(self):
+        return self.dev if self.backend == "nccl" else "cpu"
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def all_float(self, x):
+        """Per-rank scalar → list over ranks (rank order)."""
+        if self.world == 1:
+            return [float(x)]
+        t = self.torch.tensor([float(x)], dtype=self.torch.float64, device=self._cdev())
+        parts = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(parts, t)
+        return [float(p.item()) for p in parts]
+
+    def sum_int(self, x):
+        return int(round(sum(self.all_float(x))))
+
+    def gather_rows(self, t):
+        """all_gather of equally shaped per-rank tensors (checking only) → list over ranks."""
+        if self.world == 1:
+            return [t]
+        src = t.contiguous() if self.backend == "nccl" else t.contiguous().cpu()
+        parts = [self.torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src)
+        return parts
+
+
+def load_heads(P, synth, torch, cfg, B_gen, heads, dev, pin=False):
+    """Inputs of the flattened heads `heads` of a B_gen×H batch, regenerated from per-head seeds,
+    laid out [len(heads), 1, N, d] bf16 (each head its own batch entry)."""
+    N, d = cfg["N"], cfg["d"]
     spec = synth.HeadSpec(cfg["gen"], rho=cfg["rho"])
-    # weak scaling: rank r owns heads r*B*H .. (r+1)*B*H-1 of a (world·B)×H batch
-    qn, kn, vn, don = synth.make_inputs(B * world, H, N, d, seed=1234, spec=spec,
-                                        heads=range(rank * B * H, (rank + 1) * B * H))
-    host = [torch.from_numpy(x).to(torch.bfloat16).reshape(B, H, N, d).pin_memory() for x in (qn, kn, vn, don)]
-    q, k, v, do = [t.to(dev) for t in host]
-    torch.cuda.synchronize()
+    arrs = synth.make_inputs(B_gen, cfg["H"], N, d, seed=1234, spec=spec, heads=heads)
+    host = [torch.from_numpy(x).to(torch.bfloat16).reshape(len(heads), 1, N, d) for x in arrs]
+    if pin:
+        host = [h.pin_memory() for h in host]
+    return host, [h.to(dev) for h in host]
 
-    alpha, causal, n_iter = cfg["alpha"], cfg["causal"], cfg["n_iter"]
-    assert P.impl_for(q) == 1, "bench must run the tcgen05 path"
+
+def measure(P, torch, R, q, k, v, do, cfg, args, clocks=False, e2e_host=None):
+    """Time W warm-up + K steps (fwd + bwd over this rank's heads) with CUDA events on the launching
+    stream, barrier + synchronize on both sides, max over ranks; optionally a per-kernel pass (library
+    events) and the end-to-end pass through host buffers.  Returns a dict of per-rank-local facts and
+    the max-over-ranks times."""
+    alpha, causal, n_iter, N = cfg["alpha"], cfg["causal"], cfg["n_iter"], cfg["N"]
+    dev = R.dev
     fw = P.entmax_attn_fwd(q, k, v, alpha, causal, n_iter)
     ws_f = torch.empty(P.workspace_bytes(q, causal)[0], dtype=torch.uint8, device=dev)
     ws_b = torch.empty(P.workspace_bytes(q, causal)[1], dtype=torch.uint8, device=dev)
@@ -274,8 +330,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def timed(fn, steps):
-        if world > 1:
-            dist.barrier()
+        R.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -283,46 +338,54 @@ def main():
             fn()
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms / steps
+        R.barrier()
+        return e0.elapsed_time(e1) / steps
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
-
-    # ---- main timed region (device-resident inputs).  The library's per-kernel events would sit
-    # between the kernels and stop the programmatic-dependent-launch overlap, so the per-kernel
-    # breakdown comes from a second, separately timed pass.
-    with ClockSampler(local) as clk:
-        ms_step = timed(step, args.steps)
+    out = {}
+    if clocks:
+        with ClockSampler(R.local) as clk:
+            ms_local = timed(step, args.steps)
+        out["clocks"] = clk.summary()
+    else:
+        ms_local = timed(step, args.steps)
+    per_rank = R.all_float(ms_local)
+    out.update(ms=max(per_rank), per_rank_ms=per_rank)
+    # per-kernel breakdown: a second pass with the library's events between the launches (they stop
+    # the programmatic-dependent-launch overlap, so the headline above is timed without them)
     P.profile_reset()
     P.profile_enable(True)
-    ms_step_profiled = timed(step, args.steps)
+    out["ms_with_kernel_events"] = max(R.all_float(timed(step, args.steps)))
     P.profile_enable(False)
-    prof = P.profile_collect()
+    out["prof"] = P.profile_collect()
+    if e2e_host is not None:
+        out["e2e"] = e2e_pass(P, torch, R, e2e_host, (q, k, v, do), fw, grads, ws_f, ws_b, cfg, args)
+    step()
+    torch.cuda.synchronize()
+    out["pairs_local"] = visible_pairs_in_active_blocks(fw.mask, N, causal)
+    out["fw"] = fw
+    return out
 
-    # ---- e2e: every step copies its inputs host (pinned) → device and its gradients device → host,
-    # inside the timed region, through the public API.  The copies run on two copy streams (one per
-    # direction), double-buffered, so step k+1's H2D and step k's D2H overlap step k's kernels (a
-    # prefetching input pipeline); the timed region starts before the first H2D and ends after the
-    # last D2H.
+
+def e2e_pass(P, torch, R, host, dev_in, fw, grads, ws_f, ws_b, cfg, args):
+    """Every step copies its inputs host (pinned) → device and its gradients device → host inside the
+    timed region, through the public API.  Copies run on two copy streams (one per direction),
+    double-buffered, so step k+1's H2D and step k's D2H overlap step k's kernels (a prefetching input
+    pipeline); the timed region starts before the first H2D and ends after the last D2H."""
+    alpha, causal, n_iter = cfg["alpha"], cfg["causal"], cfg["n_iter"]
+    dev = R.dev
+    stream = torch.cuda.current_stream(dev)
     host_g = [[torch.empty_like(g, device="cpu").pin_memory() for g in grads] for _ in range(2)]
-    dbuf = [(q, k, v, do), tuple(torch.empty_like(t) for t in (q, k, v, do))]
+    dbuf = [tuple(dev_in), tuple(torch.empty_like(t) for t in dev_in)]
     gbuf = [grads, tuple(torch.empty_like(g) for g in grads)]
-    cstream = torch.cuda.Stream(dev)      # H2D
-    dstream = torch.cuda.Stream(dev)      # D2H (the other copy engine: both directions overlap)
+    cstream, dstream = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
-    def e2e_run(steps):
+    def run(steps):
         ev = lambda: torch.cuda.Event(enable_timing=False)
         h2d_done, comp_done, d2h_done = [ev(), ev()], [ev(), ev()], [None, None]
-        if world > 1:
-            dist.barrier()
+        R.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -359,87 +422,169 @@ def main():
         stream.wait_stream(dstream)
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev if backend == "nccl" else "cpu")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms / steps
+        R.barrier()
+        return max(R.all_float(e0.elapsed_time(e1) / steps))
 
-    e2e_run(2)
-    ms_e2e = e2e_run(max(4, args.steps))
-    h2d = sum(t.numel() * t.element_size() for t in host)
-    d2h = sum(t.numel() * t.element_size() for t in host_g[0])
+    run(2)
+    ms = run(max(4, args.steps))
     # the gradients that reached the host are the kernels' (spot check, outside the timed region)
     assert torch.equal(host_g[1][2].to(dev), gbuf[1][2]), "e2e D2H mismatch"
+    return dict(ms=ms, h2d=sum(t.numel() * t.element_size() for t in host),
+                d2h=sum(t.numel() * t.element_size() for t in host_g[0]))
 
-    # ---- accounting (outside the timed region)
-    step()
+
+def shard_check(P, synth, torch, R, cfg, heads, fw, B_gen):
+    """Outside the timed region: every rank sends τ and O of its first head to rank 0 (all_gather),
+    which regenerates those heads, runs them itself and requires the same bits — heads are independent,
+    so the split must not change any result (the oracle parity of the path is the test suite's job)."""
+    first = torch.tensor([heads[0] if len(heads) else -1], dtype=torch.int64)
+    ids = [int(x) for x in R.all_float(float(first.item()))]
+    tau_parts = R.gather_rows(fw.tau[:1].reshape(-1))
+    o_parts = R.gather_rows(fw.o[:1].reshape(-1))
+    if R.rank != 0:
+        return None
+    hs = [h for h in ids if h >= 0]
+    _, (q, k, v, _) = load_heads(P, synth, torch, cfg, B_gen, hs, R.dev)
+    ref = P.entmax_attn_fwd(q, k, v, cfg["alpha"], cfg["causal"], cfg["n_iter"])
     torch.cuda.synchronize()
-    pairs = visible_pairs_in_active_blocks(fw.mask, N, causal)
-    density = pairs / (B * H * total_visible_pairs(N, causal))
-    eff_flops_rank = 14.0 * d * pairs
-    value = eff_flops_rank * world / (ms_step * 1e-3) / 1e12
-    e2e_value = eff_flops_rank * world / (ms_e2e * 1e-3) / 1e12
-    launches_per_step = sum(n for n, _ in prof.values()) / args.steps
+    n = 0
+    for r, h in enumerate(ids):
+        if h < 0:
+            continue
+        assert torch.equal(tau_parts[r].to(R.dev), ref.tau[n].reshape(-1)), ("shard check tau", r, h)
+        assert torch.equal(o_parts[r].to(R.dev), ref.o[n].reshape(-1)), ("shard check O", r, h)
+        n += 1
+    return {"heads_checked": hs, "result": "bitwise equal to rank 0 recomputing them"}
 
-    # roofline of the dominant kernel: MMA flops it issues per launch / its mean duration
+
+def main():
+    args = parse()
+    cfg = dict(B=args.B, H=args.H, N=args.N, d=args.d, alpha=args.alpha, causal=args.causal,
+               n_iter=args.n_iter, gen=args.gen, rho=args.rho)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    maybe_reexec_under_torchrun(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2502_12082_b200 as P
+    import synth
+    from paper_2502_12082_b200.dist import imbalance, shard_heads
+
+    R = Ranks(torch, dist)
+    world, rank, dev = R.world, R.rank, R.dev
+    B, H, N, d = cfg["B"], cfg["H"], cfg["N"], cfg["d"]
+    causal = cfg["causal"]
+    scaling = args.scaling if world > 1 else "strong"
+    # SURVEY §8e: strong split = contiguous B·H/G heads per rank of the one B×H batch; weak = every rank
+    # its own B×H heads of a (G·B)×H batch.  Each rank regenerates its heads from per-head seeds.
+    if scaling == "strong":
+        B_gen, heads = B, shard_heads(B * H, world, rank)
+    else:
+        B_gen, heads = B * world, range(rank * B * H, (rank + 1) * B * H)
+    host, (q, k, v, do) = load_heads(P, synth, torch, cfg, B_gen, heads, dev, pin=True)
+    torch.cuda.synchronize()
+    assert P.impl_for(q) == 1, "bench must run the tcgen05 path"
+
+    m = measure(P, torch, R, q, k, v, do, cfg, args, clocks=True, e2e_host=host)
+    pairs = R.sum_int(m["pairs_local"])
+    total_heads = B_gen * H
+    density = pairs / (total_heads * total_visible_pairs(N, causal))
+    eff_flops = 14.0 * d * pairs                       # FA convention, non-skipped blocks only (SURVEY §8d)
+    value = eff_flops / (m["ms"] * 1e-3) / 1e12
+    e2e_value = eff_flops / (m["e2e"]["ms"] * 1e-3) / 1e12
+    prof = m["prof"]
+    launches_per_step = sum(n for n, _ in prof.values()) / args.steps
+    launches_all = R.sum_int(launches_per_step * args.steps)
+
+    # roofline of the dominant kernel (this rank's launches): MMA flops it issues per launch ÷ its mean
+    # duration (library events on the launching stream) against the measured burst bf16 peak (the
+    # timed region is well under a second, run at the clocks sampled below)
     peaks = load_peaks()
     kern_ms = {name: tot / n for name, (n, tot) in prof.items()}
     dom = max(prof, key=lambda n: prof[n][1])
-    vis_all = B * H * total_visible_pairs(N, causal)
+    pl = m["pairs_local"]
+    vis_local = len(heads) * total_visible_pairs(N, causal)
     mma_flops = {
-        # one streaming pass of S = QKᵀ + the nkb/4 warm-up tiles it re-streams (the paper's Alg. 3 would
-        # issue 1 + T passes; fallback tiers, taken by a few % of CTAs, are not counted)
-        "tau_sm100": (1.0 + (1 / 3 if d == 128 else 1 / 4)) * 2.0 * d * vis_all,   # warm-up nkb/4 (nkb/3 at d=128)
-        "out_sm100": 6.0 * d * pairs,                             # S, P·V, U·V on candidate blocks
-        "dkdv_sm100": 8.0 * d * pairs,                            # Sᵀ, dPᵀ, Pᵀ·dO, dSᵀ·Q
-        "dq_sm100": 6.0 * d * pairs,                              # S, dP, dS·K
+        # one streaming pass of S = QKᵀ + the warm-up tiles it re-streams (nkb/4, nkb/3 at d=128; the
+        # paper's Alg. 3 would issue 1 + T passes; fallback tiers, taken by a few % of CTAs, not counted)
+        "tau_sm100": (1.0 + (1 / 3 if d == 128 else 1 / 4)) * 2.0 * d * vis_local,
+        "out_sm100": 6.0 * d * pl,                             # S, P·V, U·V on candidate blocks
+        "dkdv_sm100": 8.0 * d * pl,                            # Sᵀ, dPᵀ, Pᵀ·dO, dSᵀ·Q
+        "dq_sm100": 6.0 * d * pl,                              # S, dP, dS·K
     }
+    tau_bytes = len(heads) * (N * d * 2 * (2.0 + (1 / 3 if d == 128 else 1 / 4)) + 4 * N)   # Q + 1.25 K + τ
     roof = None
     if dom in mma_flops:
         ach = mma_flops[dom] / (kern_ms[dom] * 1e-3) / 1e12
-        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peaks["bf16_sustained"],
-                "unit": "TFLOP/s", "frac": ach / peaks["bf16_sustained"], "traffic": ncu_traffic(dom),
-                "peak_src": peaks["src"] + " bf16_tflops_sustained (kernel timed inside the step)",
-                "algorithmic": "MMA flops issued per launch (see DESIGN.md §Roofline)"}
-    kernels = {n: {"launches_per_step": c / args.steps, "ms_per_launch": kern_ms[n],
-                   "share": tot / sum(t for _, t in prof.values()),
-                   **({"achieved_tflops": mma_flops[n] / (kern_ms[n] * 1e-3) / 1e12,
-                       "frac_of_sustained_bf16": mma_flops[n] / (kern_ms[n] * 1e-3) / 1e12 / peaks["bf16_sustained"],
-                       "ncu_tensor_pipe_pct": ncu_traffic(n, "tensor_pipe_pct")} if n in mma_flops else {})}
-               for n, (c, tot) in prof.items()}
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peaks["bf16"],
+                "unit": "TFLOP/s", "frac": ach / peaks["bf16"], "traffic": ncu_traffic(dom),
+                "peak_src": peaks["src"] + " bf16_tflops (burst: sub-second timed region at the sampled clocks)",
+                "algorithmic": "MMA flops issued per launch = c·d·ΣV over visible pairs of active blocks "
+                               "(c = 6 out, 8 dK/dV, 6 dQ; DESIGN.md §6)"}
+    kernels = {}
+    for n_, (c, tot) in prof.items():
+        e = {"launches_per_step": c / args.steps, "ms_per_launch": kern_ms[n_],
+             "share": tot / sum(t for _, t in prof.values())}
+        if n_ in mma_flops:
+            tf = mma_flops[n_] / (kern_ms[n_] * 1e-3) / 1e12
+            e.update(achieved_tflops=tf, frac_of_burst_bf16=tf / peaks["bf16"],
+                     ncu_tensor_pipe_pct=ncu_traffic(n_, "tensor_pipe_pct"))
+        if n_ == "tau_sm100":
+            e.update(hbm_gbs_algorithmic=tau_bytes / (kern_ms[n_] * 1e-3) / 1e9,
+                     dram_bytes_per_launch_ncu=ncu_traffic(n_))
+        kernels[n_] = e
 
+    per_rank = m["per_rank_ms"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": m["ms"], "higher_is_better": True, "scaling": scaling,
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD if (cfg["gen"] == "gaussian" and N == 8192) else
-                   f"B={B} H={H} N={N} d={d} alpha={alpha} causal={causal} n_iter={n_iter} gen={cfg['gen']} rho={cfg['rho']}",
-                   "global_batch": B * world, "heads": H, "seq_len": N, "head_dim": d, "alpha": alpha,
-                   "causal": causal, "n_iter": n_iter, "parallelism": f"heads-sharded x{world} (weak)",
-                   "l2": "inputs 201 MB/rank > 126 MB L2 (no flush)", "block_density": density},
-        "fwd_bwd_ms": ms_step, "effective_tflops": value, "ms_per_step_with_kernel_events": ms_step_profiled,
-        "gpu_launches": int(round(launches_per_step * args.steps)),
-        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": ms_e2e, "h2d_bytes_per_step": h2d,
-                "pipeline": "H2D of step k+1 and D2H of step k on two copy streams, double-buffered",
-                "d2h_bytes_per_step": d2h},
-        "roofline": roof, "kernels": kernels, "clocks": clk.summary(),
+        "config": {"workload": WORKLOAD if (cfg["gen"] == "gaussian" and N == 8192 and B == 4 and H == 12) else
+                   f"B={B} H={H} N={N} d={d} alpha={cfg['alpha']} causal={causal} n_iter={cfg['n_iter']} "
+                   f"gen={cfg['gen']} rho={cfg['rho']}",
+                   "global_batch": B_gen, "heads": H, "seq_len": N, "head_dim": d, "alpha": cfg["alpha"],
+                   "causal": causal, "n_iter": cfg["n_iter"],
+                   "parallelism": f"{total_heads} heads sharded over {world} rank(s), {scaling} "
+                                  f"({len(heads)} heads on rank {rank}), no data-path collective",
+                   "l2": f"inputs {4 * len(heads) * N * d * 2 / 1e6:.0f} MB/rank "
+                         f"{'>' if 4 * len(heads) * N * d * 2 > 126e6 else '<='} 126 MB L2 (no flush)",
+                   "block_density": density},
+        "fwd_bwd_ms": m["ms"], "effective_tflops": value, "ms_per_step_with_kernel_events": m["ms_with_kernel_events"],
+        "per_rank_ms": per_rank, "imbalance_max_over_mean": imbalance(per_rank),
+        "gpu_launches": launches_all,
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": m["e2e"]["ms"], "h2d_bytes_per_step": m["e2e"]["h2d"],
+                "d2h_bytes_per_step": m["e2e"]["d2h"],
+                "pipeline": "H2D of step k+1 and D2H of step k on two copy streams, double-buffered"},
+        "roofline": roof, "kernels": kernels, "clocks": m["clocks"],
     }
-
-    if args.sweep and rank == 0:
-        line["sweep"] = run_sweep(P, synth, torch, dev, cfg, args)
-    if args.suite and rank == 0:
-        line["suite"] = run_suite(P, synth, torch, dev, args)
-    if not args.no_rowwise and rank == 0:
-        line["next1_rowwise"] = run_rowwise(P, synth, torch, dev, peaks)
-    if args.gpt2 and rank == 0:
-        sys.path.insert(0, os.path.join(ROOT, "scripts"))
-        import gpt2_step
-        line["next4_gpt2"] = gpt2_step.run()
-
+    if world > 1:
+        line["shard_check"] = shard_check(P, synth, torch, R, cfg, list(heads), m["fw"], B_gen)
+        if scaling == "strong" and not args.no_weak:
+            # the other partition as an extra key: every rank its own B×H heads (weak scaling)
+            hw = range(rank * B * H, (rank + 1) * B * H)
+            _, (q2, k2, v2, do2) = load_heads(P, synth, torch, cfg, B * world, hw, dev)
+            del q, k, v, do
+            mw = measure(P, torch, R, q2, k2, v2, do2, cfg, args)
+            pw = R.sum_int(mw["pairs_local"])
+            line["weak"] = {"value": 14.0 * d * pw / (mw["ms"] * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": mw["ms"],
+                            "per_rank_ms": mw["per_rank_ms"], "global_batch": B * world}
+            del q2, k2, v2, do2, mw
+    del m
+    torch.cuda.empty_cache()
+    if rank == 0 and not args.no_extras:
+        if args.sweep:
+            line["sweep"] = run_sweep(P, synth, torch, dev, cfg, args)
+        if args.suite:
+            line["suite"] = run_suite(P, synth, torch, dev, args)
+        if args.fig3:
+            line["fig3_seq_len"] = run_fig3(P, synth, torch, dev, args)
+        if not args.no_rowwise:
+            line["next1_rowwise"] = run_rowwise(P, synth, torch, dev, peaks)
+        if args.gpt2:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            import gpt2_step
+            line["next4_gpt2"] = gpt2_step.run(steps=max(3, args.steps // 4), warmup=2)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, fl, desc = oracle_sample(dict(cfg), seed=0, rows=4096)
         line["cpu_baseline"] = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
@@ -447,18 +592,23 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()          # rank 0's extra lines (sweep, row-wise, CPU baseline) finish first
+        R.barrier()          # rank 0's extra lines finish first
         dist.destroy_process_group()
 
 
 def run_sweep(P, synth, torch, dev, cfg, args):
-    """Fig. 1 analogue: fwd+bwd time vs planted block density (B·H heads, same N, d, α)."""
+    """Fig. 1 analogue: fwd and fwd+bwd time vs planted block density at config 2's shape
+    (B·H heads, N, d, α), masked and unmasked; plus a ≥ 99 %-block-sparse point at N = 16384
+    (T_c = 128, ρ = 1/128: 99.2 % of the blocks skipped; the 95 / 99 % sparsity of trained models,
+    P:L976).  SDPA on the same box at ρ = 1."""
     out = []
     B, H, N, d = cfg["B"], cfg["H"], cfg["N"], cfg["d"]
-    for rho in (1.0, 0.5, 0.25, 0.1, 0.05, 0.02, 1 / 64):
+    points = [(N, r) for r in (1.0, 0.5, 0.25, 0.1, 0.05, 0.02, 1 / 64)] + [(2 * N, 1 / 128)]
+    for NN, rho in points:
         spec = synth.HeadSpec("planted", rho=rho)
-        qn, kn, vn, don = synth.make_inputs(B, H, N, d, seed=7, spec=spec)
+        qn, kn, vn, don = synth.make_inputs(B, H, NN, d, seed=7, spec=spec)
         q, k, v, do = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in (qn, kn, vn, don)]
+        del qn, kn, vn, don
         fw = P.entmax_attn_fwd(q, k, v, cfg["alpha"], cfg["causal"], cfg["n_iter"])
         g = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
 
@@ -469,18 +619,8 @@ def run_sweep(P, synth, torch, dev, cfg, args):
             f()
             P.entmax_attn_bwd(q, k, v, do, fw, cfg["alpha"], cfg["causal"], grads=g)
 
-        for _ in range(3):
-            fb()
-        torch.cuda.synchronize()
-        res = {}
-        for name, fn in (("fwd", f), ("fwd_bwd", fb)):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(max(5, args.steps // 2)):
-                fn()
-            e1.record()
-            torch.cuda.synchronize()
-            res[name] = e0.elapsed_time(e1) / max(5, args.steps // 2)
+        it = max(5, args.steps // 2)
+        res = {"fwd": _time(torch, f, it), "fwd_bwd": _time(torch, fb, it)}
         # the paper's unmasked variant (NEXT-2: every visible block, no tables) on the same inputs
         fwu = P.entmax_attn_fwd(q, k, v, cfg["alpha"], cfg["causal"], cfg["n_iter"], masked=False)
 
@@ -488,18 +628,49 @@ def run_sweep(P, synth, torch, dev, cfg, args):
             P.entmax_attn_fwd(q, k, v, cfg["alpha"], cfg["causal"], cfg["n_iter"], out=fwu, masked=False)
             P.entmax_attn_bwd(q, k, v, do, fwu, cfg["alpha"], cfg["causal"], grads=g)
 
-        res["fwd_bwd_unmasked"] = _time(torch, fbu, max(5, args.steps // 2))
+        res["fwd_bwd_unmasked"] = _time(torch, fbu, it)
         fb()
         torch.cuda.synchronize()
-        pairs = visible_pairs_in_active_blocks(fw.mask, N, cfg["causal"])
-        dens = pairs / (B * H * total_visible_pairs(N, cfg["causal"]))
-        # dense softmax reference on the same box (cuDNN / flash SDPA, FA-convention flops)
-        sd = sdpa_ms(torch, q, k, v, do, cfg["causal"]) if rho == 1.0 else None
-        out.append({"rho_target": rho, "block_density": dens, "fwd_ms": res["fwd"], "fwd_bwd_ms": res["fwd_bwd"],
+        pairs = visible_pairs_in_active_blocks(fw.mask, NN, cfg["causal"])
+        dens = pairs / (B * H * total_visible_pairs(NN, cfg["causal"]))
+        sd = sdpa_ms(torch, q, k, v, do, cfg["causal"]) if rho == 1.0 or NN != N else None
+        out.append({"N": NN, "rho_target": rho, "block_density": dens, "block_sparsity": 1.0 - dens,
+                    "fwd_ms": res["fwd"], "fwd_bwd_ms": res["fwd_bwd"],
                     "fwd_bwd_ms_unmasked": res["fwd_bwd_unmasked"],
                     "eff_tflops_fwd_bwd": 14.0 * d * pairs / (res["fwd_bwd"] * 1e-3) / 1e12,
                     **({"sdpa_fwd_bwd_ms": sd} if sd else {})})
         del q, k, v, do, fw, fwu, g
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_fig3(P, synth, torch, dev, args, lengths=(1024, 2048, 4096, 8192, 16384, 32768, 65536)):
+    """Fig. 3 analogue: non-causal attention, d = 64, α = 1.5, T = 3, Gaussian
+    inputs (query σ² = 6), sequence length 1k → 64k, fwd and fwd+bwd beside same-box SDPA.  H = 12;
+    B = max(1, 32768 / N), so every point holds ≥ 32k tokens.  Block density is measured (the paper:
+    "as context length increases, the amount of block sparsity naturally increases")."""
+    out = []
+    H, d = 12, 64
+    for N in lengths:
+        B = max(1, 32768 // N)
+        qn, kn, vn, don = synth.make_inputs(B, H, N, d, seed=33, spec=synth.HeadSpec("gaussian"))
+        q, k, v, do = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in (qn, kn, vn, don)]
+        del qn, kn, vn, don
+        fw = P.entmax_attn_fwd(q, k, v, 1.5, False, 3)
+        g = (torch.empty_like(q), torch.empty_like(k), torch.empty_like(v))
+        it = 3 if N >= 32768 else 8
+        f_ms = _time(torch, lambda: P.entmax_attn_fwd(q, k, v, 1.5, False, 3, out=fw), it)
+
+        def fb():
+            P.entmax_attn_fwd(q, k, v, 1.5, False, 3, out=fw)
+            P.entmax_attn_bwd(q, k, v, do, fw, 1.5, False, grads=g)
+        fb_ms = _time(torch, fb, it)
+        pairs = visible_pairs_in_active_blocks(fw.mask, N, False)
+        out.append({"N": N, "B": B, "H": H, "block_density": pairs / (B * H * N * N), "fwd_ms": f_ms,
+                    "fwd_bwd_ms": fb_ms, "eff_tflops_fwd_bwd": 14.0 * d * pairs / (fb_ms * 1e-3) / 1e12,
+                    "sdpa_fwd_bwd_ms": sdpa_ms(torch, q, k, v, do, False, iters=it)})
+        del q, k, v, do, fw, g
+        torch.cuda.empty_cache()
     return out
 
 
@@ -551,14 +722,20 @@ def run_rowwise(P, synth, torch, dev, peaks, rows=8192, n=8192):
 
 
 def run_suite(P, synth, torch, dev, args):
-    """BASELINE.json configs 3-5 (one line each): fwd and fwd+bwd ms and effective TFLOP/s."""
-    cases = [("config3", 8, 12, 512, 64, 1.5, False), ("config3", 8, 12, 8192, 64, 1.5, False),
-             ("config4", 8, 12, 1024, 64, 1.25, True), ("config4", 8, 12, 1024, 64, 1.5, True),
-             ("config4", 8, 12, 1024, 64, 2.0, True),
-             ("config5", 1, 16, 32768, 128, 1.5, True), ("config5", 1, 16, 65536, 128, 1.5, True)]
+    """BASELINE.json configs 3-5 (one line each, Gaussian σ² = 6 inputs) plus the planted ρ = 0.05
+    variants SURVEY §8d asks for (≈ 95 % block sparsity, the trained-model level P:L976) of config 3
+    (N = 8192) and config 5 (N = 32768): fwd and fwd+bwd ms, CUDA-graph replay, effective TFLOP/s,
+    same-box SDPA."""
+    cases = [("config3", 8, 12, 512, 64, 1.5, False, "gaussian"), ("config3", 8, 12, 8192, 64, 1.5, False, "gaussian"),
+             ("config3", 8, 12, 8192, 64, 1.5, False, "planted"),
+             ("config4", 8, 12, 1024, 64, 1.25, True, "gaussian"), ("config4", 8, 12, 1024, 64, 1.5, True, "gaussian"),
+             ("config4", 8, 12, 1024, 64, 2.0, True, "gaussian"),
+             ("config5", 1, 16, 32768, 128, 1.5, True, "gaussian"), ("config5", 1, 16, 32768, 128, 1.5, True, "planted"),
+             ("config5", 1, 16, 65536, 128, 1.5, True, "gaussian")]
     out = []
-    for name, B, H, N, d, alpha, causal in cases:
-        qn, kn, vn, don = synth.make_inputs(B, H, N, d, seed=99, spec=synth.HeadSpec("gaussian"))
+    for name, B, H, N, d, alpha, causal, gen in cases:
+        spec = synth.HeadSpec(gen, rho=0.05)
+        qn, kn, vn, don = synth.make_inputs(B, H, N, d, seed=99, spec=spec)
         q, k, v, do = [torch.from_numpy(x).to(torch.bfloat16).to(dev) for x in (qn, kn, vn, don)]
         del qn, kn, vn, don
         fw = P.entmax_attn_fwd(q, k, v, alpha, causal, 3)
@@ -587,7 +764,8 @@ def run_suite(P, synth, torch, dev, args):
             pass
         pairs = visible_pairs_in_active_blocks(fw.mask, N, causal)
         sd = sdpa_ms(torch, q, k, v, do, causal, iters=it)
-        out.append({"config": name, "B": B, "H": H, "N": N, "d": d, "alpha": alpha, "causal": causal,
+        out.append({"config": name, "gen": gen if gen == "gaussian" else "planted rho=0.05", "B": B, "H": H, "N": N,
+                    "d": d, "alpha": alpha, "causal": causal,
                     "block_density": pairs / (B * H * total_visible_pairs(N, causal)),
                     "fwd_ms": f_ms, "fwd_bwd_ms": fb_ms, "fwd_bwd_ms_cuda_graph": gms,
                     "eff_tflops_fwd": 4.0 * d * pairs / (f_ms * 1e-3) / 1e12,

@@ -55,7 +55,7 @@ struct FwdWs {
   size_t cand_cnt, cand_idx, total;
 };
 struct BwdWs {
-  size_t delta, col_cnt, col_idx, total;
+  size_t delta, col_cnt, col_idx, kbar, total;
 };
 
 FwdWs fwd_ws_layout(const entmax_shape_t& s) {
@@ -75,7 +75,9 @@ BwdWs bwd_ws_layout(const entmax_shape_t& s) {
   w.delta = 0;
   w.col_cnt = align256(BH * s.N * sizeof(float));
   w.col_idx = align256(w.col_cnt + BH * Tc * sizeof(int32_t));
-  w.total = align256(w.col_idx + BH * Tc * Tr * sizeof(int32_t));
+  // K̄_j: per-key-block mean key (fp32), written by the dK/dV kernel for dQ's leak correction (r12)
+  w.kbar = align256(w.col_idx + BH * Tc * Tr * sizeof(int32_t));
+  w.total = align256(w.kbar + BH * Tc * (size_t)s.d * sizeof(float));
   return w;
 }
 
@@ -278,7 +280,8 @@ int entmax_attn_bwd(const void* q, const void* k, const void* v, const void* o2,
     if (int rc = col_lists_launch(mask, g, col_cnt, col_idx, st)) return rc;
 
   if (impl == 1) {
-    return sm100::bwd(q, k, v, d_o, g, ap, ecode, tau, delta, row_cnt, row_idx, col_cnt, col_idx, dq, dk, dv, st);
+    return sm100::bwd(q, k, v, d_o, g, ap, ecode, tau, delta, row_cnt, row_idx, col_cnt, col_idx,
+                      (float*)(ws + wl.kbar), dq, dk, dv, st);
   }
   return simt_bwd_launch(dtype, shp->d, ecode, q, k, v, d_o, g, ap, tau, delta, row_cnt, row_idx, col_cnt, col_idx, dq,
                          dk, dv, st);

@@ -63,7 +63,7 @@ int fwd(const void* q, const void* k, const void* v, const Geom& g, const AlphaP
         int32_t* cand_idx, cudaStream_t st);
 int bwd(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap, int ecode,
         const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx, const int32_t* col_cnt,
-        const int32_t* col_idx, void* dq, void* dk, void* dv, cudaStream_t st);
+        const int32_t* col_idx, float* kbar, void* dq, void* dk, void* dv, cudaStream_t st);
 }  // namespace sm100
 
 }  // namespace entmax

@@ -20,7 +20,7 @@ constexpr size_t dkdv_smem() {
 }
 template <int D>
 constexpr size_t dq_smem() {
-  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 4 : 2) * 2 * Cfg<D>::TILE;
+  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 4 : 2) * 2 * Cfg<D>::TILE + kOnesBytes;
 }
 
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
@@ -78,7 +78,8 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
 template <int D, int E, bool CU>
 int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap,
           const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx,
-          const int32_t* col_cnt, const int32_t* col_idx, void* dq, void* dk, void* dv, cudaStream_t st) {
+          const int32_t* col_cnt, const int32_t* col_idx, float* kbar, void* dq, void* dk, void* dv,
+          cudaStream_t st) {
   CUtensorMap tq, tk, tv, tdo;
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
   {
@@ -86,7 +87,7 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
     if (int rc = set_smem(dkdv_kernel<D, E, CU>, sm)) return rc;
     ProfScope ps("dkdv_sm100", st);
     if (cudaError_t e = launch_pdl(dkdv_kernel<D, E, CU>, dim3(g.Tc, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo,
-                                   g, ap, tau, delta, col_cnt, col_idx, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
+                                   g, ap, tau, delta, col_cnt, col_idx, kbar, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
       return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
   }
   if (int rc = cuda_status("dkdv_sm100")) return rc;
@@ -95,7 +96,7 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
     if (int rc = set_smem(dq_kernel<D, E, CU>, sm)) return rc;
     ProfScope ps("dq_sm100", st);
     if (cudaError_t e = launch_pdl(dq_kernel<D, E, CU>, dim3(g.Tr, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo, g,
-                                   ap, tau, delta, row_cnt, row_idx, (__nv_bfloat16*)dq))
+                                   ap, tau, delta, row_cnt, row_idx, kbar, (__nv_bfloat16*)dq))
       return fail(ENTMAX_ERR_CUDA, "dq_sm100 launch: %s", cudaGetErrorString(e));
   }
   return cuda_status("dq_sm100");
@@ -157,9 +158,9 @@ int fwd(const void* q, const void* k, const void* v, const Geom& g, const AlphaP
 
 int bwd(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap, int ecode,
         const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx, const int32_t* col_cnt,
-        const int32_t* col_idx, void* dq, void* dk, void* dv, cudaStream_t st) {
-  return dispatch<BwdOp>(g.d, ecode, q, k, v, dO, g, ap, tau, delta, row_cnt, row_idx, col_cnt, col_idx, dq, dk, dv,
-                         st);
+        const int32_t* col_idx, float* kbar, void* dq, void* dk, void* dv, cudaStream_t st) {
+  return dispatch<BwdOp>(g.d, ecode, q, k, v, dO, g, ap, tau, delta, row_cnt, row_idx, col_cnt, col_idx, kbar, dq, dk,
+                         dv, st);
 }
 
 }  // namespace sm100

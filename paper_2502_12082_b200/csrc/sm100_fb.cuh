@@ -48,6 +48,27 @@ __device__ __forceinline__ void mma_tmem_x_tile(uint32_t d_tmem, ACol acol, cons
                      (accumulate || ks > 0) ? 1u : 0u);
 }
 
+// dQ leak correction (reading r12): a constant [16 × 128] all-ones bf16 tile (K-major SW128, two 64-column
+// chunks of 2 KB; the content is swizzle-invariant) in shared memory, so D_aux[128 × 16] += dS·Onesᵀ gives
+// every column of row i the sum ρ_i = Σ_j dŜ_ij of the bf16 dS operand exactly as the dQ MMA accumulates it.
+constexpr uint32_t kOnesRows = 16;
+constexpr uint32_t kOnesBytes = kOnesRows * 256;
+template <typename ACol>
+__device__ __forceinline__ void mma_tmem_x_ones(uint32_t d_tmem, ACol acol, const uint8_t* ones, bool accumulate) {
+  constexpr uint32_t idesc = ptx::idesc_bf16(128, kOnesRows, 0, 0);
+  const uint32_t so = ptx::smem_u32(ones);
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+    ptx::mma_bf16_ts_elect(d_tmem, acol(ks), ptx::sdesc_kmajor(so + (ks >> 2) * (kOnesRows * 128) + (ks & 3) * 32),
+                           idesc, (accumulate || ks > 0) ? 1u : 0u);
+}
+
+__device__ __forceinline__ uint4 ld_shared_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr_base_plus_idx16) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -79,6 +100,42 @@ __device__ __forceinline__ void store_row_bf16(uint32_t taddr, __nv_bfloat16* ds
       for (int e = 0; e < 32; ++e) v[e] = 0.f;
     }
     if (!do_store) continue;
+    uint4* p = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      p[q] = make_uint4(ptx::pack_bf16(v[8 * q] * scale, v[8 * q + 1] * scale),
+                        ptx::pack_bf16(v[8 * q + 2] * scale, v[8 * q + 3] * scale),
+                        ptx::pack_bf16(v[8 * q + 4] * scale, v[8 * q + 5] * scale),
+                        ptx::pack_bf16(v[8 * q + 6] * scale, v[8 * q + 7] * scale));
+  }
+}
+
+// dQ epilogue with the leak correction (reading r12): row ← c·(acc − ρ·K̄) for HALF fp32 columns, K̄ = kb[0..HALF)
+// (fp32, global), ρ this row's Σ_j dŜ_ij.
+template <int HALF>
+__device__ __forceinline__ void store_row_bf16_corr(uint32_t taddr, __nv_bfloat16* dst, float scale, bool zero,
+                                                    bool do_store, float rho, const float* __restrict__ kb) {
+#pragma unroll 1
+  for (int c = 0; c < HALF / 32; ++c) {
+    float v[32];
+    if (!zero) {
+      ld_chunk(taddr + c * 32, v);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = 0.f;
+    }
+    if (!do_store) continue;
+    if (kb != nullptr) {
+      const float4* k4 = reinterpret_cast<const float4*>(kb + c * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 kk = __ldg(k4 + q);
+        v[4 * q] = fmaf(-rho, kk.x, v[4 * q]);
+        v[4 * q + 1] = fmaf(-rho, kk.y, v[4 * q + 1]);
+        v[4 * q + 2] = fmaf(-rho, kk.z, v[4 * q + 2]);
+        v[4 * q + 3] = fmaf(-rho, kk.w, v[4 * q + 3]);
+      }
+    }
     uint4* p = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -296,7 +353,7 @@ __global__ void __launch_bounds__(kFbThreads, 1)
 dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
           const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
           const float* __restrict__ tau, const float* __restrict__ delta, const int32_t* __restrict__ row_cnt,
-          const int32_t* __restrict__ row_idx, __nv_bfloat16* __restrict__ dq) {
+          const int32_t* __restrict__ row_idx, const float* __restrict__ kbar, __nv_bfloat16* __restrict__ dq) {
   using C = Cfg<D>;
   constexpr int NST = (D == 64) ? 4 : 2;
   extern __shared__ uint8_t smem_raw[];
@@ -304,12 +361,14 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   uint8_t* sQ = smem;
   uint8_t* sDO = sQ + C::TILE;
   uint8_t* sKV = sDO + C::TILE;                 // NST × [K | V]
+  uint8_t* sOnes = sKV + NST * 2 * C::TILE;     // [16 × 128] bf16 ones (leak correction, r12)
   __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full, s_empty, ds_full, ds_empty, acc_full;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ int s_first;                       // first tile (list order) with a non-zero dS in this CTA
 
   const int i = blockIdx.x, bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long li = (long long)bh * g.Tr + i;
 
   if (threadIdx.x == 0) {
@@ -324,15 +383,19 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     ptx::mbar_init(&ds_empty, 1);
     ptx::mbar_init(&acc_full, 1);
     ptx::fence_mbar_init();
+    s_first = INT_MAX;
   }
+  for (uint32_t w = threadIdx.x; w < kOnesBytes / 4; w += blockDim.x)
+    reinterpret_cast<uint32_t*>(sOnes)[w] = 0x3f803f80u;   // bf16 1.0 pairs
+  ptx::fence_proxy_async_smem();                           // visible to the tcgen05.mma operand reads
   if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_ds = tmem + 256, t_dq = tmem + 320;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_ds = tmem + 256, t_dq = tmem + 320, t_aux = t_dq + D;
   ptx::griddep_launch_dependents();
-  ptx::griddep_wait();   // the dK/dV kernel (and everything before it) is complete
+  ptx::griddep_wait();   // the dK/dV kernel (and everything before it, incl. K̄) is complete
   const bool dense = row_idx == nullptr;   // unmasked mode: every visible key block
   const int cnt = dense ? g.visible_kblocks(i) : row_cnt[li];
   const BlockList list{dense ? nullptr : row_idx + li * g.Tc, 0};
@@ -374,6 +437,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       ptx::mbar_wait(&ds_full, k & 1);
       ptx::tc_fence_after();
       mma_tmem_x_tile<D>(t_dq, [&](int ks) { return t_ds + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
+      mma_tmem_x_ones(t_aux, [&](int ks) { return t_ds + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
       ptx::mma_commit_elect(&kv_empty[st]);
       ptx::mma_commit_elect(&ds_empty);
     }
@@ -387,6 +451,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     const float tr = valid ? tau[(long long)bh * g.N + row] : INFINITY;
     const float dl = valid ? delta[(long long)bh * g.N + row] : 0.f;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    bool seen = false;   // this warp has seen a non-zero dS (the CTA's first such tile picks K̄, r12)
     for (int k = 0; k < cnt; ++k) {
       const int jb = list[k];
       const bool masked = (jb + 1) * kBc - 1 > cta_last;
@@ -426,6 +491,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
         };
         if (masked) body(std::true_type{}); else body(std::false_type{});
       }
+      if (!seen) {   // (sign bits masked: U = 0 gives dS = ±0)
+        uint32_t orv = 0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) orv |= pd[e];
+        seen = __any_sync(0xffffffffu, (orv & 0x7fff7fffu) != 0u);
+        if (seen && lane == 0) atomicMin(&s_first, k);
+      }
       ptx::mbar_wait(&ds_empty, (k & 1) ^ 1);   // dQ(k−1) has consumed the previous dS
       ptx::tc_fence_after();
       ptx::tmem_st32(lane_base + t_ds + wg * 32, pd);
@@ -433,12 +505,25 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       ptx::tc_fence_before();
       warp_arrive(&ds_full);
     }
+    float rho = 0.f;
     if (cnt > 0) {
       ptx::mbar_wait(&acc_full, 0);
       ptx::tc_fence_after();
+      uint32_t ra[16];
+      ptx::tmem_ld16(lane_base + t_aux, ra);
+      ptx::tmem_wait_ld();
+      rho = __uint_as_float(ra[0]);
     }
-    store_row_bf16<D / 2>(lane_base + t_dq + wg * (D / 2), dq + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2),
-                          ap.scale, cnt == 0, valid);
+    // leak correction (reading r12): dQ_i = c·Σ_j dŜ_ij (K_j − K̄) = c·(acc_i − ρ_i·K̄), exact in real
+    // arithmetic for any K̄ because Σ_j dS_ij = 0 (definition of δ); K̄ = mean key of the
+    // CTA's first block with a non-zero dS removes the rounding leak's component along the support's keys
+    ptx::named_bar_sync(1, kFbMath);
+    const int kf = s_first;
+    const float* kb = (kf == INT_MAX || kbar == nullptr) ? nullptr
+                      : kbar + ((long long)bh * g.Tc + list[kf]) * D + wg * (D / 2);
+    store_row_bf16_corr<D / 2>(lane_base + t_dq + wg * (D / 2),
+                               dq + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2), ap.scale, cnt == 0, valid,
+                               rho, kb);
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -458,7 +543,8 @@ __global__ void __launch_bounds__(kFbThreads, 1)
 dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
             const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
             const float* __restrict__ tau, const float* __restrict__ delta, const int32_t* __restrict__ col_cnt,
-            const int32_t* __restrict__ col_idx, __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv) {
+            const int32_t* __restrict__ col_idx, float* __restrict__ kbar, __nv_bfloat16* __restrict__ dk,
+            __nv_bfloat16* __restrict__ dv) {
   using C = Cfg<D>;
   constexpr bool ALIAS = (D == 128);
   constexpr int NST = (D == 64) ? 3 : 2;
@@ -631,6 +717,35 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
     const long long off = g.head_off(bh) + (long long)(valid ? key : 0) * g.sn + wg * (D / 2);
     store_row_bf16<D / 2>(lane_base + t_dv + wg * (D / 2), dv + off, 1.0f, cnt == 0, valid);
     store_row_bf16<D / 2>(lane_base + t_dk + wg * (D / 2), dk + off, ap.scale, cnt == 0, valid);
+    if (kbar != nullptr) {
+      // K̄_j = mean of the block's keys (fp32) for the dQ kernel's leak correction (reading r12), from the
+      // K tile this CTA holds in shared memory (rows past N are TMA zero fill).  Thread → (16-byte unit u of
+      // a row, row phase rp); partial sums reduced through the (now idle) stage buffers.
+      constexpr int UNITS = D / 8, RP = kFbMath / UNITS;
+      ptx::mbar_wait(&bar_kv, 0);
+      const int u = tid % UNITS, rp = tid / UNITS;
+      const uint32_t kb0 = ptx::smem_u32(sK) + (uint32_t)(u >> 3) * kChunkBytes;
+      float a[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = 0.f;
+#pragma unroll 4
+      for (int rr = rp; rr < 128; rr += RP) {
+        const uint4 w = ld_shared_u4(kb0 + ptx::sw128_off(rr, u & 7));
+        const float2 f0 = bf16x2_to_float2(w.x), f1 = bf16x2_to_float2(w.y), f2 = bf16x2_to_float2(w.z),
+                     f3 = bf16x2_to_float2(w.w);
+        a[0] += f0.x; a[1] += f0.y; a[2] += f1.x; a[3] += f1.y;
+        a[4] += f2.x; a[5] += f2.y; a[6] += f3.x; a[7] += f3.y;
+      }
+      float* red = reinterpret_cast<float*>(sStage);   // [RP][D]
+#pragma unroll
+      for (int e = 0; e < 8; ++e) red[rp * D + u * 8 + e] = a[e];
+      ptx::named_bar_sync(1, kFbMath);
+      if (tid < D) {
+        float sum = 0.f;
+        for (int p = 0; p < RP; ++p) sum += red[p * D + tid];
+        kbar[((long long)bh * g.Tc + j) * D + tid] = sum / (float)min(kBc, g.N - j * kBc);
+      }
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();

@@ -38,3 +38,10 @@ def gather_heads(local: torch.Tensor, n_heads: int, device=None) -> torch.Tensor
     parts = [torch.empty((s,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device) for s in sizes]
     dist.all_gather(parts, local.contiguous())
     return torch.cat(parts, 0) if rank == 0 else None
+
+
+def imbalance(per_rank_ms) -> float:
+    """max/mean of the per-rank step times (1.0 = perfectly balanced; heads of different block
+    density make the ranks' work differ)."""
+    t = [float(x) for x in per_rank_ms]
+    return max(t) / (sum(t) / len(t))

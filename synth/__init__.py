@@ -22,6 +22,11 @@ any code.  Recipes (DESIGN.md §"Input recipe"):
   Keys keep a Gaussian spread around their cluster direction (a near-constant
   key set would make dQ = Σ dS·K a near-total cancellation).
 
+* ``planted_tight`` — SURVEY App. P3's original recipe, kept as a stress case: the same planted block
+  structure with near-duplicate keys and queries, Q = a·u_c + 0.02·N(0,1), owned K = a·u_c + 0.02·N(0,1)
+  (dead K = N(0,1)).  Rows see hundreds of nearly equal scores and dQ = c·Σ_j dS_ij K_j is an almost
+  total cancellation (real attention sees repeated tokens; reading r12).
+
 * ``step``      — Gaussian with the first half of the keys scaled by 0.2 (structure test for the
   τ kernel's list-overflow tiers; no paper workload).
 
@@ -34,7 +39,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["head_rng", "gaussian_head", "planted_head", "step_head", "make_inputs", "HeadSpec", "rowwise_scores"]
+__all__ = ["head_rng", "gaussian_head", "planted_head", "planted_tight_head", "step_head", "make_inputs", "HeadSpec", "rowwise_scores"]
 
 
 def head_rng(seed: int, b: int, h: int, stream: int = 0) -> np.random.Generator:
@@ -93,6 +98,37 @@ def planted_head(N: int, d: int, rho: float, seed: int, b: int = 0, h: int = 0,
     return f32(q), f32(k), f32(v), f32(do), owned
 
 
+def planted_tight_head(N: int, d: int, rho: float, seed: int, b: int = 0, h: int = 0,
+                       Br: int = 128, Bc: int = 128, gap: float = 12.0, noise: float = 0.02):
+    """SURVEY App. P3 planted head with near-duplicate keys/queries (see module doc).  Same cluster
+    bookkeeping as planted_head; returns (q, k, v, do, owned)."""
+    rng = head_rng(seed, b, h, stream=3)
+    Tr = (N + Br - 1) // Br
+    Tc = (N + Bc - 1) // Bc
+    m = min(max(1, int(round(rho * Tc))), Tc)
+    C = max(1, min(8, d // 4, Tc // m, Tr))
+    qmat, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    u = qmat[:, :C].T.astype(np.float64)
+    a = np.sqrt(gap * np.sqrt(d))
+    perm = rng.permutation(Tc)
+    cluster_blocks = [np.sort(perm[c * m:(c + 1) * m]) for c in range(C)]
+    qc = rng.integers(0, C, size=Tr)
+    q = np.empty((N, d), dtype=np.float64)
+    for i in range(Tr):
+        r0, r1 = i * Br, min(N, (i + 1) * Br)
+        q[r0:r1] = a * u[qc[i]] + noise * rng.standard_normal((r1 - r0, d))
+    k = rng.standard_normal((N, d))
+    for c in range(C):
+        for j in cluster_blocks[c]:
+            c0, c1 = j * Bc, min(N, (j + 1) * Bc)
+            k[c0:c1] = a * u[c] + noise * rng.standard_normal((c1 - c0, d))
+    v = rng.standard_normal((N, d))
+    do = rng.standard_normal((N, d))
+    owned = [cluster_blocks[qc[i]] for i in range(Tr)]
+    f32 = lambda x: x.astype(np.float32)
+    return f32(q), f32(k), f32(v), f32(do), owned
+
+
 def step_head(N: int, d: int, seed: int, b: int = 0, h: int = 0, sigma2_q: float = 6.0, low: float = 0.2):
     """Gaussian head whose first ⌊N/2⌋ keys are scaled by ``low``: their scores are bunched far below
     the row maxima, which all sit in the second half.  A structure test for streaming τ solvers
@@ -114,6 +150,8 @@ class HeadSpec:
             return gaussian_head(N, d, seed, b, h, self.sigma2_q)
         if self.kind == "planted":
             return planted_head(N, d, self.rho, seed, b, h, self.Br, self.Bc)[:4]
+        if self.kind == "planted_tight":
+            return planted_tight_head(N, d, self.rho, seed, b, h, self.Br, self.Bc)[:4]
         if self.kind == "step":
             return step_head(N, d, seed, b, h, self.sigma2_q)
         raise ValueError(f"unknown generator kind {self.kind!r}")

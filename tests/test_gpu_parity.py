@@ -282,3 +282,18 @@ def test_padded_layout_qkv_split(causal):
         check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
     fc, gc = run_gpu(dev, 1.5, causal, 3)                   # same bits as the contiguous layout
     assert torch.equal(fc.o, fw.o) and all(torch.equal(a, b) for a, b in zip(gc, grads))
+
+
+@pytest.mark.parametrize("N,causal,d", [(1024, False, 64), (1024, True, 64), (768, False, 128)])
+def test_parity_near_duplicate_keys(N, causal, d):
+    """SURVEY App. P3's original planted recipe (synth 'planted_tight': queries and owned keys
+    a·u_c + 0.02·N(0,1)): rows see hundreds of near-equal scores and dQ = c·Σ_j dS_ij K_j cancels to
+    ~2 % of its terms, so the bf16 rounding leak of dS must be removed (reading r12: ρ_i·K̄ correction)
+    for dQ to meet the 3e-2 bar.  Everything else is checked at the usual bars."""
+    _require_gpu()
+    spec = synth.HeadSpec("planted_tight", rho=0.25)
+    dev, ref = make_case(1, 2, N, d, torch.bfloat16, seed=41 + d, spec=spec)
+    fw, grads = run_gpu(dev, 1.5, causal, 3)
+    for bh in range(2):
+        out = check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
+        assert out["dQ"] <= 1e-2, out
