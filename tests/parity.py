@@ -40,7 +40,7 @@ def rel_l2(a, b, floor_rms=1e-4):
 # fraction of query rows allowed to carry near-tie alternatives (reading r10): a converged run
 # (T >= 3, the paper's setting) has almost none; with T < 3 the unconverged iteration is close to a
 # decision on more rows
-MAX_FLAGGED = {True: 0.02, False: 0.5}
+MAX_FLAGGED = {True: 0.05, False: 0.5}
 
 
 def mirror_tau(q, k, alpha, causal, n_iter, tau_gpu, rows=None, report=None):
