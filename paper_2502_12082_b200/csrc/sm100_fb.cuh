@@ -15,6 +15,7 @@
 #include <type_traits>
 
 #include "sm100_kernels.cuh"
+#include "trace.cuh"
 
 namespace entmax {
 namespace sm100 {
@@ -575,6 +576,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
     ptx::mbar_init(&acc_full, 1);
     ptx::fence_mbar_init();
   }
+  if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8002);
   if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
   ptx::tc_fence_before();
   __syncthreads();
@@ -601,6 +603,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       const int ib = list[k], st = k % NST;
       uint8_t* stg = sStage + st * STAGE;
       ptx::mbar_wait(&qd_empty[st], ((k / NST) & 1) ^ 1);
+      ENTMAX_TRACE_K(2, 8 * k + 7);
       float* tq_s = reinterpret_cast<float*>(stg + 2 * C::TILE);
       float* dl_s = tq_s + 128;
 #pragma unroll
@@ -631,6 +634,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
       mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
       ptx::mma_commit_elect(&s_full);
+      ENTMAX_TRACE_K(2, 8 * k + 0);
     };
     if (cnt > 0) issue_sdp(0);
     for (int k = 0; k < cnt; ++k) {
@@ -638,6 +642,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       const int st = k % NST;
       const uint8_t* stg = sStage + st * STAGE;
       ptx::mbar_wait(&p_full, k & 1);
+      ENTMAX_TRACE_K(2, 8 * k + 1);
       ptx::tc_fence_after();
       mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
       mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
@@ -646,6 +651,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       if (ALIAS && k + 1 < cnt) issue_sdp(k + 1);
     }
     ptx::mma_commit_elect(&acc_full);
+    ENTMAX_TRACE_K(2, 8001);
   } else {
     const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
     const int key = j * kBc + r;
@@ -659,6 +665,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       const bool diag = g.causal && ib == j;   // queries below the key inside the diagonal block
       ptx::mbar_wait(&qd_full[st], (k / NST) & 1);   // τ_i, δ_i staged by the producer warp
       ptx::mbar_wait(&s_full, k & 1);
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 3);
       ptx::tc_fence_after();
       uint32_t pp[32], pd[32];
 #pragma unroll
@@ -700,16 +707,20 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
         };
         if (!valid || diag) body(std::true_type{}); else body(std::false_type{});
       }
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 4);
       if (!ALIAS) {
         ptx::mbar_wait(&p_empty, (k & 1) ^ 1);   // dV/dK(k−1) have consumed the previous Pᵀ, dSᵀ
         ptx::tc_fence_after();
       }
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 5);
       ptx::tmem_st32(lane_base + pt_col(wg * 4), pp);
       ptx::tmem_st32(lane_base + dst_col(wg * 4), pd);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       warp_arrive(&p_full);
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 6);
     }
+    if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8000);
     if (cnt > 0) {
       ptx::mbar_wait(&acc_full, 0);
       ptx::tc_fence_after();
@@ -749,6 +760,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8003);
   if (warp == 9) ptx::tmem_dealloc<512>(tmem);
 }
 
