@@ -193,6 +193,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     ptx::fence_mbar_init();
   }
   for (int j = threadIdx.x; j < g.Tc; j += blockDim.x) aflag[j] = 0;
+  if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8002);
   if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
   ptx::tc_fence_before();
   __syncthreads();
@@ -214,6 +215,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     for (int k = 0; k < ncand; ++k) {
       const int j = list[k], st = k % NST;
       ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+      ENTMAX_TRACE_K(1, 8 * k + 7);
 #ifdef ENTMAX_FB_HALFTMA   // diagnostics: half the streamed bytes (results invalid)
       ptx::mbar_arrive_expect_tx_elect(&kv_full[st], C::TILE);
       tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], j * kBc, h, b);
@@ -231,12 +233,14 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::tc_fence_after();
       mma_rows_x_rows<D>(tmem + (k & 1) * 128, sQ, sKV + st * 2 * C::TILE, false);
       ptx::mma_commit_elect(&s_full[k & 1]);
+      ENTMAX_TRACE_K(1, 8 * k + 0);
     };
     if (ncand > 0) issue_s(0);
     if (ncand > 1) issue_s(1);
     for (int k = 0; k < ncand; ++k) {
       const int st = k % NST, sb = k & 1;
       ptx::mbar_wait(&p_full[sb], (k >> 1) & 1);
+      ENTMAX_TRACE_K(1, 8 * k + 1);
       ptx::tc_fence_after();
       const uint32_t buf = tmem + sb * 128;
       const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
@@ -260,6 +264,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       const bool masked = (j + 1) * kBc - 1 > cta_last;
       const uint32_t col = lane_base + sb * 128 + wg * 64;
       ptx::mbar_wait(&s_full[sb], (k >> 1) & 1);
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 3);
       ptx::tc_fence_after();
       float s0[32], s1[32];
       ld32f_nowait(col, s0);
@@ -293,11 +298,13 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       if (masked) body(std::true_type{}); else body(std::false_type{});
       usum += su.x + su.y;
       if (E == 1 || E == 2) xmax = su.x + su.y;   // exact: every U > 0 iff x > 0 (no underflow for e <= 2)
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 4);
       ptx::tmem_st32(col, pp);
       if (TRAIN) ptx::tmem_st32(col + 32, pu);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       warp_arrive(&p_full[sb]);
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 6);
       if (__any_sync(0xffffffffu, xmax > 0.f) && lane == 0) aflag[j] = 1;
     }
     // epilogue: O and O⁽²⁾ = (Σ U V)/ΣU; each column half written by its warpgroup
@@ -340,6 +347,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8003);
   if (warp == 9) ptx::tmem_dealloc<512>(tmem);
 }
 
@@ -389,6 +397,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   for (uint32_t w = threadIdx.x; w < kOnesBytes / 4; w += blockDim.x)
     reinterpret_cast<uint32_t*>(sOnes)[w] = 0x3f803f80u;   // bf16 1.0 pairs
   ptx::fence_proxy_async_smem();                           // visible to the tcgen05.mma operand reads
+  if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8002);
   if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
   ptx::tc_fence_before();
   __syncthreads();
@@ -410,6 +419,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     for (int k = 0; k < cnt; ++k) {
       const int jb = list[k], st = k % NST;
       ptx::mbar_wait(&kv_empty[st], ((k / NST) & 1) ^ 1);
+      ENTMAX_TRACE_K(3, 8 * k + 7);
 #ifdef ENTMAX_FB_HALFTMA
       ptx::mbar_arrive_expect_tx_elect(&kv_full[st], C::TILE);
       tma_tile<D>(sKV + st * 2 * C::TILE, &tk, &kv_full[st], jb * kBc, h, b);
@@ -430,12 +440,14 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
       mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
       ptx::mma_commit_elect(&s_full);
+      ENTMAX_TRACE_K(3, 8 * k + 0);
     };
     if (cnt > 0) issue_sdp(0);
     for (int k = 0; k < cnt; ++k) {
       if (k + 1 < cnt) issue_sdp(k + 1);
       const int st = k % NST;
       ptx::mbar_wait(&ds_full, k & 1);
+      ENTMAX_TRACE_K(3, 8 * k + 1);
       ptx::tc_fence_after();
       mma_tmem_x_tile<D>(t_dq, [&](int ks) { return t_ds + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
       mma_tmem_x_ones(t_aux, [&](int ks) { return t_ds + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
@@ -458,19 +470,25 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       const bool masked = (jb + 1) * kBc - 1 > cta_last;
       const int key0 = jb * kBc + wg * 64;
       ptx::mbar_wait(&s_full, k & 1);
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 3);
       ptx::tc_fence_after();
       uint32_t pd[32];
       const float2 cp2 = make_float2(ap.cp, ap.cp), ntr2 = make_float2(-tr, -tr), ndl2 = make_float2(-dl, -dl);
+      // all 64 columns of S and dP at once: the buffers are released right after one TMEM latency, so
+      // S/dP(k+1) run on the tensor pipe while this warp computes tile k
+      float sa[2][32], da[2][32];
+      ld32f_nowait(lane_base + t_s + wg * 64, sa[0]);
+      ld32f_nowait(lane_base + t_dp + wg * 64, da[0]);
+      ld32f_nowait(lane_base + t_s + wg * 64 + 32, sa[1]);
+      ld32f_nowait(lane_base + t_dp + wg * 64 + 32, da[1]);
+      ptx::tmem_wait_ld();
+      ptx::tc_fence_before();
+      warp_arrive(&s_empty);
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 4);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        float s[32], dp[32];
-        ld32f_nowait(lane_base + t_s + wg * 64 + hh * 32, s);
-        ld32f_nowait(lane_base + t_dp + wg * 64 + hh * 32, dp);
-        ptx::tmem_wait_ld();
-        if (hh == 1) {
-          ptx::tc_fence_before();
-          warp_arrive(&s_empty);
-        }
+        const float(&s)[32] = sa[hh];
+        const float(&dp)[32] = da[hh];
         auto body = [&](auto masked_c) {
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
@@ -500,11 +518,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
         if (seen && lane == 0) atomicMin(&s_first, k);
       }
       ptx::mbar_wait(&ds_empty, (k & 1) ^ 1);   // dQ(k−1) has consumed the previous dS
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 5);
       ptx::tc_fence_after();
       ptx::tmem_st32(lane_base + t_ds + wg * 32, pd);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       warp_arrive(&ds_full);
+      if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 6);
     }
     float rho = 0.f;
     if (cnt > 0) {
@@ -528,6 +548,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8003);
   if (warp == 9) ptx::tmem_dealloc<512>(tmem);
 }
 
@@ -668,16 +689,22 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 3);
       ptx::tc_fence_after();
       uint32_t pp[32], pd[32];
+      // all 64 columns of Sᵀ and dPᵀ are read at once, so the MMA warp can start Sᵀ/dPᵀ(k+1) while this
+      // warp still computes tile k (one wait instead of two; the buffers are free ~a TMEM latency in)
+      float sa[2][32], da[2][32];
+      ld32f_nowait(lane_base + t_s + wg * 64, sa[0]);
+      ld32f_nowait(lane_base + t_dp + wg * 64, da[0]);
+      ld32f_nowait(lane_base + t_s + wg * 64 + 32, sa[1]);
+      ld32f_nowait(lane_base + t_dp + wg * 64 + 32, da[1]);
+      ptx::tmem_wait_ld();
+      if (!ALIAS) {
+        ptx::tc_fence_before();
+        warp_arrive(&s_empty);
+      }
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        float s[32], dp[32];
-        ld32f_nowait(lane_base + t_s + wg * 64 + hh * 32, s);
-        ld32f_nowait(lane_base + t_dp + wg * 64 + hh * 32, dp);
-        ptx::tmem_wait_ld();
-        if (!ALIAS && hh == 1) {
-          ptx::tc_fence_before();
-          warp_arrive(&s_empty);
-        }
+        const float(&s)[32] = sa[hh];
+        const float(&dp)[32] = da[hh];
         auto body = [&](auto masked_c) {
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4) {
