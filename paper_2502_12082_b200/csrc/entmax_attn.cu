@@ -55,7 +55,7 @@ struct FwdWs {
   size_t cand_cnt, cand_idx, total;
 };
 struct BwdWs {
-  size_t delta, col_cnt, col_idx, kbar, total;
+  size_t delta, col_cnt, col_idx, kbar, td, total;
 };
 
 FwdWs fwd_ws_layout(const entmax_shape_t& s) {
@@ -77,7 +77,9 @@ BwdWs bwd_ws_layout(const entmax_shape_t& s) {
   w.col_idx = align256(w.col_cnt + BH * Tc * sizeof(int32_t));
   // K̄_j: per-key-block mean key (fp32), written by the dK/dV kernel for dQ's leak correction (r12)
   w.kbar = align256(w.col_idx + BH * Tc * Tr * sizeof(int32_t));
-  w.total = align256(w.kbar + BH * Tc * (size_t)s.d * sizeof(float));
+  // td: per query block {τ[128] | δ[128]} (+∞ / 0 past N), the dK/dV producer's bulk-copy source
+  w.td = align256(w.kbar + BH * Tc * (size_t)s.d * sizeof(float));
+  w.total = align256(w.td + BH * Tr * 2 * kBr * sizeof(float));
   return w;
 }
 
@@ -275,12 +277,13 @@ int entmax_attn_bwd(const void* q, const void* k, const void* v, const void* o2,
 
   // δ and the 𝒦 tables — shared by both implementations; the unmasked
   // mode visits every visible block and needs no tables
-  if (int rc = delta_launch(dtype, d_o, o2, g, delta, st)) return rc;
+  float* td = impl == 1 ? (float*)(ws + wl.td) : nullptr;
+  if (int rc = delta_launch(dtype, d_o, o2, tau, g, delta, td, st)) return rc;
   if (!unmasked)
     if (int rc = col_lists_launch(mask, g, col_cnt, col_idx, st)) return rc;
 
   if (impl == 1) {
-    return sm100::bwd(q, k, v, d_o, g, ap, ecode, tau, delta, row_cnt, row_idx, col_cnt, col_idx,
+    return sm100::bwd(q, k, v, d_o, g, ap, ecode, tau, delta, row_cnt, row_idx, col_cnt, col_idx, td,
                       (float*)(ws + wl.kbar), dq, dk, dv, st);
   }
   return simt_bwd_launch(dtype, shp->d, ecode, q, k, v, d_o, g, ap, tau, delta, row_cnt, row_idx, col_cnt, col_idx, dq,

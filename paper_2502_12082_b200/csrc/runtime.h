@@ -52,7 +52,8 @@ int simt_bwd_launch(int dtype, int d, int ecode, const void* q, const void* k, c
                     const int32_t* row_cnt, const int32_t* row_idx, const int32_t* col_cnt, const int32_t* col_idx,
                     void* dq, void* dk, void* dv, cudaStream_t st);
 // shared small kernels (simt.cu)
-int delta_launch(int dtype, const void* dO, const void* o2, const Geom& g, float* delta, cudaStream_t st);
+int delta_launch(int dtype, const void* dO, const void* o2, const float* tau, const Geom& g, float* delta, float* td,
+                 cudaStream_t st);
 int col_lists_launch(const uint8_t* mask, const Geom& g, int32_t* col_cnt, int32_t* col_idx, cudaStream_t st);
 
 // tcgen05 path (sm100.cu)
@@ -63,7 +64,7 @@ int fwd(const void* q, const void* k, const void* v, const Geom& g, const AlphaP
         int32_t* cand_idx, cudaStream_t st);
 int bwd(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap, int ecode,
         const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx, const int32_t* col_cnt,
-        const int32_t* col_idx, float* kbar, void* dq, void* dk, void* dv, cudaStream_t st);
+        const int32_t* col_idx, const float* td, float* kbar, void* dq, void* dk, void* dv, cudaStream_t st);
 }  // namespace sm100
 
 }  // namespace entmax

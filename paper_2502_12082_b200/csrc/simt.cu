@@ -96,26 +96,29 @@ int simt_bwd_launch(int dtype, int d, int ecode, const void* q, const void* k, c
 }
 
 template <typename T>
-static void delta_go(const T* dO, const float* o2, const Geom& g, float* delta, cudaStream_t st) {
-  const long long rows = (long long)g.B * g.H * g.N;
+static void delta_go(const T* dO, const float* o2, const float* tau, const Geom& g, float* delta, float* td,
+                     cudaStream_t st) {
+  const long long rows = (long long)g.B * g.H * g.Tr * kBr;   // padded rows (td staging)
   const int tpr = g.d / 8;
   const unsigned blocks = (unsigned)((rows * tpr + 255) / 256);
   switch (tpr) {
-    case 2: launch_pdl(delta_kernel<T, 2>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
-    case 4: launch_pdl(delta_kernel<T, 4>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
-    case 8: launch_pdl(delta_kernel<T, 8>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
-    default: launch_pdl(delta_kernel<T, 16>, dim3(blocks), dim3(256), 0, st, dO, o2, g, delta); break;
+    case 2: launch_pdl(delta_kernel<T, 2>, dim3(blocks), dim3(256), 0, st, dO, o2, tau, g, delta, td); break;
+    case 4: launch_pdl(delta_kernel<T, 4>, dim3(blocks), dim3(256), 0, st, dO, o2, tau, g, delta, td); break;
+    case 8: launch_pdl(delta_kernel<T, 8>, dim3(blocks), dim3(256), 0, st, dO, o2, tau, g, delta, td); break;
+    default: launch_pdl(delta_kernel<T, 16>, dim3(blocks), dim3(256), 0, st, dO, o2, tau, g, delta, td); break;
   }
 }
 
-int delta_launch(int dtype, const void* dO, const void* o2, const Geom& g, float* delta, cudaStream_t st) {
+int delta_launch(int dtype, const void* dO, const void* o2, const float* tau, const Geom& g, float* delta, float* td,
+                 cudaStream_t st) {
   if (g.d != 16 && g.d != 32 && g.d != 64 && g.d != 128) return fail(ENTMAX_ERR_UNSUPPORTED, "delta: d = %d not supported", g.d);
   {
     ProfScope ps("delta", st);
     if (dtype == ENTMAX_FP32)
-      delta_go<float>(static_cast<const float*>(dO), static_cast<const float*>(o2), g, delta, st);
+      delta_go<float>(static_cast<const float*>(dO), static_cast<const float*>(o2), tau, g, delta, td, st);
     else
-      delta_go<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(dO), static_cast<const float*>(o2), g, delta, st);
+      delta_go<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(dO), static_cast<const float*>(o2), tau, g, delta, td,
+                              st);
   }
   return cuda_status("delta");
 }

@@ -316,27 +316,39 @@ __device__ __forceinline__ void load8<float>(const float* p, float (&v)[8]) {
 }
 
 template <typename T, int TPR>
-__global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, const float* __restrict__ o2, Geom g,
-                                                    float* __restrict__ delta) {
+__global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, const float* __restrict__ o2,
+                                                    const float* __restrict__ tau, Geom g, float* __restrict__ delta,
+                                                    float* __restrict__ td) {
+  // δ_i = dO_i · O⁽²⁾_i.  With td != NULL (tcgen05 path) also the per-query-block staging array
+  // td[bh][i] = {τ of the block's 128 rows | δ of them} (1 KB, +∞ / 0 past N) that the dK/dV kernel's
+  // producer pulls with one bulk copy per query block; rows run over the padded T_r·128 rows per head.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");   // (launched with PDL: see runtime.h)
-  const long long row = ((long long)blockIdx.x * 256 + threadIdx.x) / TPR;
+  const long long prow = ((long long)blockIdx.x * 256 + threadIdx.x) / TPR;
   const int sub = threadIdx.x % TPR;
-  const long long total = (long long)g.B * g.H * g.N;
-  const bool ok = row < total;
+  const long long rows_pad = (long long)g.B * g.H * g.Tr * kBr;
+  const bool in = prow < rows_pad;
+  const int bh = in ? (int)(prow / ((long long)g.Tr * kBr)) : 0;
+  const int r = in ? (int)(prow - (long long)bh * g.Tr * kBr) : 0;
+  const bool ok = in && r < g.N;
   float s = 0.f;
   if (ok) {
-    const int bh = (int)(row / g.N);
-    const int r = (int)(row - (long long)bh * g.N);
     float a[8], b[8];
     load8<T>(dO + g.head_off(bh) + (long long)r * g.sn + sub * 8, a);
-    load8<float>(o2 + row * g.d + sub * 8, b);   // fp32 contiguous [B,H,N,d]
+    load8<float>(o2 + ((long long)bh * g.N + r) * g.d + sub * 8, b);   // fp32 contiguous [B,H,N,d]
 #pragma unroll
     for (int e = 0; e < 8; ++e) s = fmaf(a[e], b[e], s);
   }
 #pragma unroll
   for (int m = TPR / 2; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-  if (ok && sub == 0) delta[row] = s;
+  if (in && sub == 0) {
+    if (ok) delta[(long long)bh * g.N + r] = s;
+    if (td != nullptr) {
+      float* blk = td + ((long long)bh * g.Tr + r / kBr) * (2 * kBr);
+      blk[r % kBr] = ok ? tau[(long long)bh * g.N + r] : INFINITY;
+      blk[kBr + r % kBr] = ok ? s : 0.f;
+    }
+  }
 }
 
 // 𝒦_j = {i | M_ij = 1} from the mask, increasing i; one thread per (head, j).

@@ -78,7 +78,7 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
 template <int D, int E, bool CU>
 int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap,
           const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx,
-          const int32_t* col_cnt, const int32_t* col_idx, float* kbar, void* dq, void* dk, void* dv,
+          const int32_t* col_cnt, const int32_t* col_idx, const float* td, float* kbar, void* dq, void* dk, void* dv,
           cudaStream_t st) {
   CUtensorMap tq, tk, tv, tdo;
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
@@ -87,7 +87,7 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
     if (int rc = set_smem(dkdv_kernel<D, E, CU>, sm)) return rc;
     ProfScope ps("dkdv_sm100", st);
     if (cudaError_t e = launch_pdl(dkdv_kernel<D, E, CU>, dim3(g.Tc, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo,
-                                   g, ap, tau, delta, col_cnt, col_idx, kbar, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
+                                   g, ap, td, col_cnt, col_idx, kbar, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
       return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
   }
   if (int rc = cuda_status("dkdv_sm100")) return rc;
@@ -158,9 +158,9 @@ int fwd(const void* q, const void* k, const void* v, const Geom& g, const AlphaP
 
 int bwd(const void* q, const void* k, const void* v, const void* dO, const Geom& g, const AlphaParams& ap, int ecode,
         const float* tau, const float* delta, const int32_t* row_cnt, const int32_t* row_idx, const int32_t* col_cnt,
-        const int32_t* col_idx, float* kbar, void* dq, void* dk, void* dv, cudaStream_t st) {
-  return dispatch<BwdOp>(g.d, ecode, q, k, v, dO, g, ap, tau, delta, row_cnt, row_idx, col_cnt, col_idx, kbar, dq, dk,
-                         dv, st);
+        const int32_t* col_idx, const float* td, float* kbar, void* dq, void* dk, void* dv, cudaStream_t st) {
+  return dispatch<BwdOp>(g.d, ecode, q, k, v, dO, g, ap, tau, delta, row_cnt, row_idx, col_cnt, col_idx, td, kbar, dq,
+                         dk, dv, st);
 }
 
 }  // namespace sm100

@@ -150,11 +150,11 @@ __device__ __forceinline__ void store_row_bf16_corr(uint32_t taddr, __nv_bfloat1
 // =====================================================================================
 // Output pass (Alg. 2 over the candidate blocks, App. B.3): S = Q K_jᵀ → x = c'·s − τ,
 // P = [x]_+^e, U = [x]_+^{e−1}; O += P V_j, O⁽²⁾ += U V_j (TRAIN); M_ij = any(x > 0).
-// TMEM: two S buffers [0,256) — after the math warps read a buffer they overwrite their own
-// 64 columns with P (cols wg·64 + [0,32)) and U (wg·64 + [32,64)) — O at 256, O⁽²⁾ at 256 + D.
-// The MMA issue order S(0) S(1) | PV(0) UV(0) S(2) | PV(1) UV(1) S(3) … keeps the tensor pipe on
-// the next tile while the math warps work on the current one; S(k+2) is issued after PV(k) in
-// program order, so the in-order tensor pipe never overwrites P(k) before it is consumed.
+// TMEM: NSB S buffers of 128 columns (3 at d = 64, 2 at d = 128 in training) — after the math warps read
+// a buffer they overwrite their own 64 columns with P (cols wg·64 + [0,32)) and U (wg·64 + [32,64)) —
+// then O and O⁽²⁾.  The MMA issue order S(0) … S(NSB−1) | PV(0) UV(0) S(NSB) | PV(1) UV(1) S(NSB+1) …
+// keeps the tensor pipe on later tiles while the math warps work on the current one; S(k+NSB) is issued
+// after PV(k) in program order, so the in-order tensor pipe never overwrites P(k) before it is consumed.
 // =====================================================================================
 template <int D, int E, bool TRAIN, bool CU>
 __global__ void __launch_bounds__(kFbThreads, 1)
@@ -165,13 +165,17 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
            int32_t* __restrict__ row_idx) {
   using C = Cfg<D>;
   constexpr int NST = (D == 64) ? 4 : 2;
+  // S buffers in TMEM (P/U overwrite their own S buffer): three where the accumulators leave room
+  // (d = 64: 3 × 128 + O 64 + O⁽²⁾ 64; inference d = 128: 3 × 128 + O 128), so S(k+3) runs while the math
+  // warps still work on tiles k+1 and k+2
+  constexpr int NSB = (D == 64 || !TRAIN) ? 3 : 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + C::TILE;                  // NST × [K tile | V tile]
   float* xch = reinterpret_cast<float*>(sKV + NST * 2 * C::TILE);   // [256]
   uint8_t* aflag = reinterpret_cast<uint8_t*>(xch + kFbMath);       // [Tc]
-  __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full[2], p_full[2], o_full;
+  __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full[NSB], p_full[NSB], o_full;
   __shared__ uint32_t tmem_base_sh;
 
   const int i = blockIdx.x, bh = blockIdx.y;
@@ -185,7 +189,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NSB; ++s) {
       ptx::mbar_init(&s_full[s], 1);
       ptx::mbar_init(&p_full[s], 8);
     }
@@ -199,7 +203,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t t_o = tmem + 256, t_o2 = tmem + 256 + D;
+  const uint32_t t_o = tmem + 128 * NSB, t_o2 = t_o + D;
   ptx::griddep_launch_dependents();
   ptx::griddep_wait();   // the τ kernel's outputs are complete and visible
   const bool dense = mask == nullptr;   // unmasked mode: every visible block, no mask / table output
@@ -231,15 +235,14 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       const int st = k % NST;
       ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
       ptx::tc_fence_after();
-      mma_rows_x_rows<D>(tmem + (k & 1) * 128, sQ, sKV + st * 2 * C::TILE, false);
-      ptx::mma_commit_elect(&s_full[k & 1]);
+      mma_rows_x_rows<D>(tmem + (k % NSB) * 128, sQ, sKV + st * 2 * C::TILE, false);
+      ptx::mma_commit_elect(&s_full[k % NSB]);
       ENTMAX_TRACE_K(1, 8 * k + 0);
     };
-    if (ncand > 0) issue_s(0);
-    if (ncand > 1) issue_s(1);
+    for (int k = 0; k < NSB && k < ncand; ++k) issue_s(k);
     for (int k = 0; k < ncand; ++k) {
-      const int st = k % NST, sb = k & 1;
-      ptx::mbar_wait(&p_full[sb], (k >> 1) & 1);
+      const int st = k % NST, sb = k % NSB;
+      ptx::mbar_wait(&p_full[sb], (k / NSB) & 1);
       ENTMAX_TRACE_K(1, 8 * k + 1);
       ptx::tc_fence_after();
       const uint32_t buf = tmem + sb * 128;
@@ -247,7 +250,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
       if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
       ptx::mma_commit_elect(&kv_empty[st]);
-      if (k + 2 < ncand) issue_s(k + 2);
+      if (k + NSB < ncand) issue_s(k + NSB);
     }
     ptx::mma_commit_elect(&o_full);
   } else {
@@ -260,10 +263,10 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     float usum = 0.f;
     for (int k = 0; k < ncand; ++k) {
-      const int j = list[k], sb = k & 1;
+      const int j = list[k], sb = k % NSB;
       const bool masked = (j + 1) * kBc - 1 > cta_last;
       const uint32_t col = lane_base + sb * 128 + wg * 64;
-      ptx::mbar_wait(&s_full[sb], (k >> 1) & 1);
+      ptx::mbar_wait(&s_full[sb], (k / NSB) & 1);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 3);
       ptx::tc_fence_after();
       float s0[32], s1[32];
@@ -315,14 +318,14 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::mbar_wait(&o_full, 0);
       ptx::tc_fence_after();
     }
-    store_row_bf16<D / 2>(lane_base + 256 + wg * (D / 2), o + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2),
+    store_row_bf16<D / 2>(lane_base + 128 * NSB + wg * (D / 2), o + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2),
                           1.0f, ncand == 0, valid);
     if (TRAIN) {
 #pragma unroll 1
       for (int c = 0; c < D / 64; ++c) {
         float v[32];
         if (ncand > 0) {
-          ld_chunk(lane_base + 256 + D + wg * (D / 2) + c * 32, v);
+          ld_chunk(lane_base + 128 * NSB + D + wg * (D / 2) + c * 32, v);
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = 0.f;
@@ -365,13 +368,14 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
           const int32_t* __restrict__ row_idx, const float* __restrict__ kbar, __nv_bfloat16* __restrict__ dq) {
   using C = Cfg<D>;
   constexpr int NST = (D == 64) ? 4 : 2;
+  constexpr int NDS = (D == 64) ? 2 : 1;   // dS buffers in TMEM: the math warps write dS(k+1) while dQ(k) runs
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sDO = sQ + C::TILE;
   uint8_t* sKV = sDO + C::TILE;                 // NST × [K | V]
   uint8_t* sOnes = sKV + NST * 2 * C::TILE;     // [16 × 128] bf16 ones (leak correction, r12)
-  __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full, s_empty, ds_full, ds_empty, acc_full;
+  __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full, s_empty, ds_full[NDS], ds_empty[NDS], acc_full;
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_first;                       // first tile (list order) with a non-zero dS in this CTA
 
@@ -388,8 +392,10 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     }
     ptx::mbar_init(&s_full, 1);
     ptx::mbar_init(&s_empty, 8);
-    ptx::mbar_init(&ds_full, 8);
-    ptx::mbar_init(&ds_empty, 1);
+    for (int s = 0; s < NDS; ++s) {
+      ptx::mbar_init(&ds_full[s], 8);
+      ptx::mbar_init(&ds_empty[s], 1);
+    }
     ptx::mbar_init(&acc_full, 1);
     ptx::fence_mbar_init();
     s_first = INT_MAX;
@@ -403,7 +409,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
-  const uint32_t t_s = tmem, t_dp = tmem + 128, t_ds = tmem + 256, t_dq = tmem + 320, t_aux = t_dq + D;
+  // TMEM: S [0,128), dP [128,256), dS buffers 64 each from 256, dQ (D), ρ aux (16)
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_ds = tmem + 256, t_dq = tmem + 256 + 64 * NDS, t_aux = t_dq + D;
   ptx::griddep_launch_dependents();
   ptx::griddep_wait();   // the dK/dV kernel (and everything before it, incl. K̄) is complete
   const bool dense = row_idx == nullptr;   // unmasked mode: every visible key block
@@ -446,13 +453,15 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     for (int k = 0; k < cnt; ++k) {
       if (k + 1 < cnt) issue_sdp(k + 1);
       const int st = k % NST;
-      ptx::mbar_wait(&ds_full, k & 1);
+      const int db = k % NDS;
+      const uint32_t dsb = t_ds + 64 * db;
+      ptx::mbar_wait(&ds_full[db], (k / NDS) & 1);
       ENTMAX_TRACE_K(3, 8 * k + 1);
       ptx::tc_fence_after();
-      mma_tmem_x_tile<D>(t_dq, [&](int ks) { return t_ds + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
-      mma_tmem_x_ones(t_aux, [&](int ks) { return t_ds + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
+      mma_tmem_x_tile<D>(t_dq, [&](int ks) { return dsb + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
+      mma_tmem_x_ones(t_aux, [&](int ks) { return dsb + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
       ptx::mma_commit_elect(&kv_empty[st]);
-      ptx::mma_commit_elect(&ds_empty);
+      ptx::mma_commit_elect(&ds_empty[db]);
     }
     ptx::mma_commit_elect(&acc_full);
   } else {
@@ -517,13 +526,14 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
         seen = __any_sync(0xffffffffu, (orv & 0x7fff7fffu) != 0u);
         if (seen && lane == 0) atomicMin(&s_first, k);
       }
-      ptx::mbar_wait(&ds_empty, (k & 1) ^ 1);   // dQ(k−1) has consumed the previous dS
+      const int db = k % NDS;
+      ptx::mbar_wait(&ds_empty[db], ((k / NDS) & 1) ^ 1);   // dQ(k−NDS) has consumed this dS buffer
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 5);
       ptx::tc_fence_after();
-      ptx::tmem_st32(lane_base + t_ds + wg * 32, pd);
+      ptx::tmem_st32(lane_base + t_ds + 64 * db + wg * 32, pd);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      warp_arrive(&ds_full);
+      warp_arrive(&ds_full[db]);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 6);
     }
     float rho = 0.f;
@@ -564,7 +574,7 @@ template <int D, int E, bool CU>
 __global__ void __launch_bounds__(kFbThreads, 1)
 dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
             const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
-            const float* __restrict__ tau, const float* __restrict__ delta, const int32_t* __restrict__ col_cnt,
+            const float* __restrict__ td, const int32_t* __restrict__ col_cnt,
             const int32_t* __restrict__ col_idx, float* __restrict__ kbar, __nv_bfloat16* __restrict__ dk,
             __nv_bfloat16* __restrict__ dv) {
   using C = Cfg<D>;
@@ -625,24 +635,13 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       uint8_t* stg = sStage + st * STAGE;
       ptx::mbar_wait(&qd_empty[st], ((k / NST) & 1) ^ 1);
       ENTMAX_TRACE_K(2, 8 * k + 7);
-      float* tq_s = reinterpret_cast<float*>(stg + 2 * C::TILE);
-      float* dl_s = tq_s + 128;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int rr = ib * kBr + lane * 4 + e;
-        tq_s[lane * 4 + e] = rr < g.N ? tau[(long long)bh * g.N + rr] : INFINITY;
-        dl_s[lane * 4 + e] = rr < g.N ? delta[(long long)bh * g.N + rr] : 0.f;
-      }
-      __syncwarp();
-#ifdef ENTMAX_FB_HALFTMA
-      ptx::mbar_arrive_expect_tx_elect(&qd_full[st], C::TILE);
-      tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
-#else
-      ptx::mbar_arrive_expect_tx_elect(&qd_full[st], 2 * C::TILE);
+      // τ_i and δ_i of the block's 128 rows (+∞ / 0 past N) with one bulk copy from the staging array the
+      // δ kernel wrote — asynchronous like the tiles, so the producer never waits on a global load
+      ENTMAX_TRACE_K(2, 4224 + k);
+      ptx::mbar_arrive_expect_tx_elect(&qd_full[st], 2 * C::TILE + 2 * kBr * 4);
+      ptx::bulk_load_elect(stg + 2 * C::TILE, td + ((long long)bh * g.Tr + ib) * (2 * kBr), 2 * kBr * 4, &qd_full[st]);
       tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
       tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
-#endif
-      __syncwarp();
     }
   } else if (warp == 9) {
     ptx::mbar_wait(&bar_kv, 0);
@@ -650,7 +649,9 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       const int st = k % NST;
       const uint8_t* stg = sStage + st * STAGE;
       ptx::mbar_wait(&qd_full[st], (k / NST) & 1);
+      ENTMAX_TRACE_K(2, 4096 + k);
       if (!ALIAS) ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
+      ENTMAX_TRACE_K(2, 4160 + k);
       ptx::tc_fence_after();
       mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
       mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
@@ -701,6 +702,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
         ptx::tc_fence_before();
         warp_arrive(&s_empty);
       }
+      if (lane == 0) ENTMAX_TRACE_K(2, 4288 + 8 * k + warp);
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const float(&s)[32] = sa[hh];

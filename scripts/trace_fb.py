@@ -43,3 +43,13 @@ print("median: math s_full->compute done", np.median((math_ld - math_start)[ok])
       " arrive->next s_full", np.median(math_start[1:][ok[1:]] - math_end[:-1][ok[1:]]))
 print("median MMA: p_full seen after math arrive", np.median((mma_p - math_end)[ok & (mma_p >= 0)]))
 print("tile period (math_end diff)", np.median(np.diff(math_end[ok])))
+if kid == 2:
+    qf = b[4096:4096 + n]; se = b[4160:4160 + n]; pt = b[4224:4224 + n]
+    wa = b[4288:4288 + 8 * n].reshape(n, 8)
+    print("k  prod_tma  mma_qdfull  mma_sempty  sdp_issued | warp s_empty arrivals (min..max)")
+    for kk in list(range(0, 5)) + list(range(30, 35)) + list(range(n - 4, n - 1)):
+        print(f"{kk:3d} {pt[kk]:9d} {qf[kk]:10d} {se[kk]:10d} {b[8 * kk]:10d} | {wa[kk].min():9d} .. {wa[kk].max():9d}")
+    ok = slice(2, n - 2)
+    print("median: prod TMA issue -> qd_full seen", np.median(qf[ok] - pt[ok]),
+          " qd_full -> s_empty passed", np.median(se[ok] - qf[ok]),
+          " warp arrive spread", np.median(wa[ok].max(1) - wa[ok].min(1)))
