@@ -133,6 +133,31 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   return d;
 }
 
+__device__ __forceinline__ float2 fabs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+// two floats → bf16x2 (RN) with relu: one F2FP.RELU; lo lands in the low half
+__device__ __forceinline__ uint32_t pack_relu_bf16(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+// P̂ = bf16([x]_+^e) and Û = bf16([x]_+^{e−1}) for e ∈ {2, 4} straight from x, without a separate relu:
+// sign-carrying powers (x·|x|, …: the |·| is a free FMUL2 operand modifier) and relu inside the pack.
+// Bitwise the same values as p_and_u + pack (x·|x| = x·x for x > 0; x <= 0 packs to ±0).
+template <int E>
+__device__ __forceinline__ void pu_packed(float2 x, uint32_t& pb, uint32_t& ub) {
+  static_assert(E == 2 || E == 4, "integer exponents 2, 4");
+  const float2 a = fmul2(x, fabs2(x));                 // x|x|  (= x² for x > 0)
+  if constexpr (E == 2) {
+    pb = pack_relu_bf16(a.x, a.y);
+    ub = pack_relu_bf16(x.x, x.y);
+  } else {
+    const float2 b = fmul2(a, fabs2(x));               // x³ with x's sign
+    const float2 c = fmul2(a, fabs2(a));               // x⁴ with x's sign
+    pb = pack_relu_bf16(c.x, c.y);
+    ub = pack_relu_bf16(b.x, b.y);
+  }
+}
+
 // Generic α: U = x^{e−1} = 2^{(e−1)·log2 x} and P = U·x for a pair of x with two
 // MUFU ops per element (lg2.approx.ftz, ex2.approx.ftz) and three other instructions, instead of an
 // accurate exp2f per power (the tensor-core kernels are issue-bound there, so the instruction count is

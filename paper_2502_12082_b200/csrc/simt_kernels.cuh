@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, co
   // δ_i = dO_i · O⁽²⁾_i.  With td != NULL (tcgen05 path) also the per-query-block staging array
   // td[bh][i] = {τ of the block's 128 rows | δ of them} (1 KB, +∞ / 0 past N) that the dK/dV kernel's
   // producer pulls with one bulk copy per query block; rows run over the padded T_r·128 rows per head.
+  // Padding rows get τ = 1e10 (finite: x = c′s − τ then gives exact zeros through x + |x|) and δ = 0.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");   // (launched with PDL: see runtime.h)
   const long long prow = ((long long)blockIdx.x * 256 + threadIdx.x) / TPR;
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(256) delta_kernel(const T* __restrict__ dO, co
     if (ok) delta[(long long)bh * g.N + r] = s;
     if (td != nullptr) {
       float* blk = td + ((long long)bh * g.Tr + r / kBr) * (2 * kBr);
-      blk[r % kBr] = ok ? tau[(long long)bh * g.N + r] : INFINITY;
+      blk[r % kBr] = ok ? tau[(long long)bh * g.N + r] : 1e10f;   // (finite: see sm100_fb.cuh kPadTau)
       blk[kBr + r % kBr] = ok ? s : 0.f;
     }
   }

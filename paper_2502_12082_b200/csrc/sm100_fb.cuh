@@ -35,6 +35,12 @@ __device__ __forceinline__ uint32_t mul_bf16x2(uint32_t a, uint32_t b) {
   return d;
 }
 
+// Invisible (causal) keys and padding rows: large finite values instead of ±∞, so the sign-carrying
+// power forms (x + |x|, x·|x|, … in pu_packed and the doubled dS) give exact zeros instead of ∞ − ∞.
+// Every visible x = c′·s − τ is many orders of magnitude smaller.
+constexpr float kMaskX = -1e10f;    // x of an invisible key
+constexpr float kPadTau = 1e10f;    // τ of a row past N
+
 constexpr int kFbThreads = 320;
 constexpr int kFbMath = 256;
 
@@ -259,7 +265,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const bool valid = row < g.N;
     const int my_last = g.causal ? row : g.N - 1;
     const int cta_last = g.causal ? i * kBr : g.N - 1;
-    const float tr = valid ? tau[(long long)bh * g.N + row] : INFINITY;
+    const float tr = valid ? tau[(long long)bh * g.N + row] : kPadTau;
     const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     float usum = 0.f;
     for (int k = 0; k < ncand; ++k) {
@@ -283,22 +289,40 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         for (int e = 0; e < 64; e += 2) {
           float2 x = ffma2(make_float2(e < 32 ? s0[e] : s1[e - 32], e < 32 ? s0[e + 1] : s1[e - 31]), cp2, ntr2);
           if constexpr (decltype(masked_c)::value) {
-            if (key0 + e > my_last) x.x = -INFINITY;
-            if (key0 + e + 1 > my_last) x.y = -INFINITY;
+            if (key0 + e > my_last) x.x = kMaskX;
+            if (key0 + e + 1 > my_last) x.y = kMaskX;
           }
           if (E != 1 && E != 2) xmax = fmaxf(xmax, fmaxf(x.x, x.y));
-          float2 p, u;
-          p_and_u2<E>(x, ap, p, u);
-          // U enters the U·V MMA rounded to bf16 (c14); with CU, ‖U‖₁ is summed from the same rounded
-          // values (reading r9)
-          const uint32_t ub = ptx::pack_bf16(u.x, u.y);
-          if constexpr (CU) su = fadd2(su, bf16x2_to_float2(ub));
-          else su = fadd2(su, u);
-          pp[e >> 1] = ptx::pack_bf16(p.x, p.y);
-          pu[e >> 1] = ub;
+          if constexpr (E == 2 || E == 4) {
+            // P̂, Û packed straight from x (pu_packed); ΣU from 2u = x + |x| (E = 2) or b + |b| (E = 4),
+            // exact doublings, halved at the end — bitwise the same sums as Σ relu(·)
+            uint32_t pb, ub;
+            pu_packed<E>(x, pb, ub);
+            if constexpr (CU) {
+              su = fadd2(su, bf16x2_to_float2(ub));   // ‖Û‖₁ of the rounded U the U·V MMA sees (r9)
+            } else if constexpr (E == 2) {
+              su = fadd2(su, fadd2(x, fabs2(x)));
+            } else {
+              const float2 b = fmul2(fmul2(x, fabs2(x)), fabs2(x));
+              su = fadd2(su, fadd2(b, fabs2(b)));
+            }
+            pp[e >> 1] = pb;
+            pu[e >> 1] = ub;
+          } else {
+            float2 p, u;
+            p_and_u2<E>(x, ap, p, u);
+            // U enters the U·V MMA rounded to bf16 (c14); with CU, ‖U‖₁ is summed from the same rounded
+            // values (reading r9)
+            const uint32_t ub = ptx::pack_bf16(u.x, u.y);
+            if constexpr (CU) su = fadd2(su, bf16x2_to_float2(ub));
+            else su = fadd2(su, u);
+            pp[e >> 1] = ptx::pack_bf16(p.x, p.y);
+            pu[e >> 1] = ub;
+          }
         }
       };
       if (masked) body(std::true_type{}); else body(std::false_type{});
+      if constexpr ((E == 2 || E == 4) && !CU) su = fmul2(su, make_float2(0.5f, 0.5f));
       usum += su.x + su.y;
       if (E == 1 || E == 2) xmax = su.x + su.y;   // exact: every U > 0 iff x > 0 (no underflow for e <= 2)
       if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 4);
@@ -368,7 +392,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
           const int32_t* __restrict__ row_idx, const float* __restrict__ kbar, __nv_bfloat16* __restrict__ dq) {
   using C = Cfg<D>;
   constexpr int NST = (D == 64) ? 4 : 2;
-  constexpr int NDS = (D == 64) ? 2 : 1;   // dS buffers in TMEM: the math warps write dS(k+1) while dQ(k) runs
+  constexpr int NDS = (D == 64) ? 2 : 1;
+  constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dS is kDS·dS (exact doubling)   // dS buffers in TMEM: the math warps write dS(k+1) while dQ(k) runs
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
@@ -470,7 +495,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     const bool valid = row < g.N;
     const int my_last = g.causal ? row : g.N - 1;
     const int cta_last = g.causal ? i * kBr : g.N - 1;
-    const float tr = valid ? tau[(long long)bh * g.N + row] : INFINITY;
+    const float tr = valid ? tau[(long long)bh * g.N + row] : kPadTau;
     const float dl = valid ? delta[(long long)bh * g.N + row] : 0.f;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     bool seen = false;   // this warp has seen a non-zero dS (the CTA's first such tile picks K̄, r12)
@@ -503,17 +528,30 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
           for (int e = 0; e < 32; e += 2) {
             float2 x = ffma2(make_float2(s[e], s[e + 1]), cp2, ntr2);
             if constexpr (decltype(masked_c)::value) {
-              if (key0 + hh * 32 + e > my_last) x.x = -INFINITY;
-              if (key0 + hh * 32 + e + 1 > my_last) x.y = -INFINITY;
+              if (key0 + hh * 32 + e > my_last) x.x = kMaskX;
+              if (key0 + hh * 32 + e + 1 > my_last) x.y = kMaskX;
             }
-            float2 p, u;
-            p_and_u2<E>(x, ap, p, u);
             const float2 g2 = fadd2(make_float2(dp[e], dp[e + 1]), ndl2);
-            if constexpr (CU)   // Û (r9)
-              pd[hh * 16 + (e >> 1)] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
-            else {
-              const float2 ds = fmul2(u, g2);
-              pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+            if constexpr (E == 2 || E == 4) {
+              if constexpr (CU) {   // Û (r9)
+                uint32_t pb, ub;
+                pu_packed<E>(x, pb, ub);
+                pd[hh * 16 + (e >> 1)] = mul_bf16x2(ub, ptx::pack_bf16(g2.x, g2.y));
+              } else {
+                // 2dS = (2u)·(dP − δ), 2u = x + |x| (E = 2) or b + |b|, b = x³ signed: exact doubling, no relu
+                const float2 b = E == 2 ? x : fmul2(fmul2(x, fabs2(x)), fabs2(x));
+                const float2 ds2 = fmul2(fadd2(b, fabs2(b)), g2);
+                pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(ds2.x, ds2.y);
+              }
+            } else {
+              float2 p, u;
+              p_and_u2<E>(x, ap, p, u);
+              if constexpr (CU)   // Û (r9)
+                pd[hh * 16 + (e >> 1)] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
+              else {
+                const float2 ds = fmul2(u, g2);
+                pd[hh * 16 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+              }
             }
           }
         };
@@ -553,7 +591,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     const float* kb = (kf == INT_MAX || kbar == nullptr) ? nullptr
                       : kbar + ((long long)bh * g.Tc + list[kf]) * D + wg * (D / 2);
     store_row_bf16_corr<D / 2>(lane_base + t_dq + wg * (D / 2),
-                               dq + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2), ap.scale, cnt == 0, valid,
+                               dq + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2), ap.scale / kDS, cnt == 0,
+                               valid,
                                rho, kb);
   }
   ptx::tc_fence_before();
@@ -581,6 +620,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   constexpr bool ALIAS = (D == 128);
   constexpr int NST = (D == 64) ? 3 : 2;
   constexpr uint32_t STAGE = 2 * C::TILE + 1024;   // Q_i | dO_i | τ_i[128] | δ_i[128]
+  constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dSᵀ is kDS·dSᵀ (exact doubling)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sK = smem;
@@ -718,18 +758,31 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
               float2 x = ffma2(make_float2(s[q4 * 4 + e], s[q4 * 4 + e + 1]), make_float2(ap.cp, ap.cp), tq2);
               if constexpr (decltype(masked_c)::value) {
                 const int ql = wg * 64 + hh * 32 + q4 * 4 + e;
-                if (!valid || (diag && ql < r)) x.x = -INFINITY;
-                if (!valid || (diag && ql + 1 < r)) x.y = -INFINITY;
+                if (!valid || (diag && ql < r)) x.x = kMaskX;
+                if (!valid || (diag && ql + 1 < r)) x.y = kMaskX;
               }
-              float2 p, u;
-              p_and_u2<E>(x, ap, p, u);
               const float2 g2 = fadd2(make_float2(dp[q4 * 4 + e], dp[q4 * 4 + e + 1]), dq2);
-              pp[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(p.x, p.y);
-              if constexpr (CU)   // Û (r9)
-                pd[hh * 16 + q4 * 2 + (e >> 1)] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
-              else {
-                const float2 ds = fmul2(u, g2);
-                pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+              if constexpr (E == 2 || E == 4) {
+                uint32_t pb, ub;
+                pu_packed<E>(x, pb, ub);
+                pp[hh * 16 + q4 * 2 + (e >> 1)] = pb;
+                if constexpr (CU) {   // Û (r9)
+                  pd[hh * 16 + q4 * 2 + (e >> 1)] = mul_bf16x2(ub, ptx::pack_bf16(g2.x, g2.y));
+                } else {   // 2dSᵀ = (2u)·(dPᵀ − δ): exact doubling, no relu (see the dQ kernel)
+                  const float2 bb = E == 2 ? x : fmul2(fmul2(x, fabs2(x)), fabs2(x));
+                  const float2 ds2 = fmul2(fadd2(bb, fabs2(bb)), g2);
+                  pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds2.x, ds2.y);
+                }
+              } else {
+                float2 p, u;
+                p_and_u2<E>(x, ap, p, u);
+                pp[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(p.x, p.y);
+                if constexpr (CU)   // Û (r9)
+                  pd[hh * 16 + q4 * 2 + (e >> 1)] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
+                else {
+                  const float2 ds = fmul2(u, g2);
+                  pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+                }
               }
             }
           }
@@ -756,7 +809,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
     }
     const long long off = g.head_off(bh) + (long long)(valid ? key : 0) * g.sn + wg * (D / 2);
     store_row_bf16<D / 2>(lane_base + t_dv + wg * (D / 2), dv + off, 1.0f, cnt == 0, valid);
-    store_row_bf16<D / 2>(lane_base + t_dk + wg * (D / 2), dk + off, ap.scale, cnt == 0, valid);
+    store_row_bf16<D / 2>(lane_base + t_dk + wg * (D / 2), dk + off, ap.scale / kDS, cnt == 0, valid);
     if (kbar != nullptr) {
       // K̄_j = mean of the block's keys (fp32) for the dQ kernel's leak correction (reading r12), from the
       // K tile this CTA holds in shared memory (rows past N are TMA zero fill).  Thread → (16-byte unit u of
