@@ -12,15 +12,15 @@ namespace {
 
 template <int D>
 constexpr size_t out_smem(int Tc) {
-  return 1024 + Cfg<D>::TILE + ((D == 64) ? 4 : 2) * 2 * Cfg<D>::TILE + kFbMath * 4 + (size_t)Tc;
+  return 1024 + Cfg<D>::TILE + ((D == 64) ? 6 : 2) * 2 * Cfg<D>::TILE + kFbMath * 4 + (size_t)Tc;
 }
 template <int D>
 constexpr size_t dkdv_smem() {
-  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 3 : 2) * (2 * Cfg<D>::TILE + 1024);
+  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 5 : 2) * (2 * Cfg<D>::TILE + 1024);
 }
 template <int D>
 constexpr size_t dq_smem() {
-  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 4 : 2) * 2 * Cfg<D>::TILE + kOnesBytes;
+  return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 5 : 2) * 2 * Cfg<D>::TILE + kOnesBytes;
 }
 
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100

@@ -170,7 +170,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
            float* __restrict__ o2, uint8_t* __restrict__ mask, int32_t* __restrict__ row_cnt,
            int32_t* __restrict__ row_idx) {
   using C = Cfg<D>;
-  constexpr int NST = (D == 64) ? 4 : 2;
+  constexpr int NST = (D == 64) ? 6 : 2;    // K/V stages (d = 64: 6 × 32 KB, deep enough to cover the TMA latency)
   // S buffers in TMEM (P/U overwrite their own S buffer): three where the accumulators leave room
   // (d = 64: 3 × 128 + O 64 + O⁽²⁾ 64; inference d = 128: 3 × 128 + O 128), so S(k+3) runs while the math
   // warps still work on tiles k+1 and k+2
@@ -236,27 +236,33 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 #endif
     }
   } else if (warp == 9) {
+    // Event-driven issue (two independent streams, one thread of control): P·V/U·V of the oldest tile
+    // whose P/U are written, else S of the next tile once its K/V stage has landed and its S buffer's
+    // previous P/U are consumed (S(k) is issued after PV(k − NSB) in program order; the in-order tensor
+    // pipe then never overwrites unread P/U).  A late TMA stage never holds up the P·V of ready tiles.
     ptx::mbar_wait(&bar_q, 0);
-    auto issue_s = [&](int k) {
-      const int st = k % NST;
-      ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
-      ptx::tc_fence_after();
-      mma_rows_x_rows<D>(tmem + (k % NSB) * 128, sQ, sKV + st * 2 * C::TILE, false);
-      ptx::mma_commit_elect(&s_full[k % NSB]);
-      ENTMAX_TRACE_K(1, 8 * k + 0);
-    };
-    for (int k = 0; k < NSB && k < ncand; ++k) issue_s(k);
-    for (int k = 0; k < ncand; ++k) {
-      const int st = k % NST, sb = k % NSB;
-      ptx::mbar_wait(&p_full[sb], (k / NSB) & 1);
-      ENTMAX_TRACE_K(1, 8 * k + 1);
-      ptx::tc_fence_after();
-      const uint32_t buf = tmem + sb * 128;
-      const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
-      mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
-      if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
-      ptx::mma_commit_elect(&kv_empty[st]);
-      if (k + NSB < ncand) issue_s(k + NSB);
+    int ns = 0, npv = 0;
+    while (npv < ncand) {
+      if (npv < ns && ptx::mbar_test(&p_full[npv % NSB], (npv / NSB) & 1)) {
+        const int k = npv, st = k % NST, sb = k % NSB;
+        ENTMAX_TRACE_K(1, 8 * k + 1);
+        ptx::tc_fence_after();
+        const uint32_t buf = tmem + sb * 128;
+        const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
+        mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+        if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+        ptx::mma_commit_elect(&kv_empty[st]);
+        ++npv;
+      } else if (ns < ncand && ns < npv + NSB && ptx::mbar_test(&kv_full[ns % NST], (ns / NST) & 1)) {
+        const int k = ns, st = k % NST;
+        ptx::tc_fence_after();
+        mma_rows_x_rows<D>(tmem + (k % NSB) * 128, sQ, sKV + st * 2 * C::TILE, false);
+        ptx::mma_commit_elect(&s_full[k % NSB]);
+        ENTMAX_TRACE_K(1, 8 * k + 0);
+        ++ns;
+      } else {
+        __nanosleep(32);   // yield the SMSP's issue slots to the math warps while nothing is ready
+      }
     }
     ptx::mma_commit_elect(&o_full);
   } else {
@@ -391,7 +397,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
           const float* __restrict__ tau, const float* __restrict__ delta, const int32_t* __restrict__ row_cnt,
           const int32_t* __restrict__ row_idx, const float* __restrict__ kbar, __nv_bfloat16* __restrict__ dq) {
   using C = Cfg<D>;
-  constexpr int NST = (D == 64) ? 4 : 2;
+  constexpr int NST = (D == 64) ? 5 : 2;   // K/V stages
   constexpr int NDS = (D == 64) ? 2 : 1;
   constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dS is kDS·dS (exact doubling)   // dS buffers in TMEM: the math warps write dS(k+1) while dQ(k) runs
   extern __shared__ uint8_t smem_raw[];
@@ -462,31 +468,34 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
 #endif
     }
   } else if (warp == 9) {
+    // Event-driven issue: dQ(k) (+ ρ) as soon as dS(k) is written, else S/dP of the next tile once its
+    // K/V stage has landed and the math warps have read the previous S/dP (they read all of it first)
     ptx::mbar_wait(&bar_q, 0);
-    auto issue_sdp = [&](int k) {
-      const int st = k % NST;
-      const uint8_t* sK = sKV + st * 2 * C::TILE;
-      ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
-      ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
-      ptx::tc_fence_after();
-      mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
-      mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
-      ptx::mma_commit_elect(&s_full);
-      ENTMAX_TRACE_K(3, 8 * k + 0);
-    };
-    if (cnt > 0) issue_sdp(0);
-    for (int k = 0; k < cnt; ++k) {
-      if (k + 1 < cnt) issue_sdp(k + 1);
-      const int st = k % NST;
-      const int db = k % NDS;
-      const uint32_t dsb = t_ds + 64 * db;
-      ptx::mbar_wait(&ds_full[db], (k / NDS) & 1);
-      ENTMAX_TRACE_K(3, 8 * k + 1);
-      ptx::tc_fence_after();
-      mma_tmem_x_tile<D>(t_dq, [&](int ks) { return dsb + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
-      mma_tmem_x_ones(t_aux, [&](int ks) { return dsb + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
-      ptx::mma_commit_elect(&kv_empty[st]);
-      ptx::mma_commit_elect(&ds_empty[db]);
+    int ns = 0, nq = 0;
+    while (nq < cnt) {
+      if (nq < ns && ptx::mbar_test(&ds_full[nq % NDS], (nq / NDS) & 1)) {
+        const int k = nq, st = k % NST, db = k % NDS;
+        const uint32_t dsb = t_ds + 64 * db;
+        ENTMAX_TRACE_K(3, 8 * k + 1);
+        ptx::tc_fence_after();
+        mma_tmem_x_tile<D>(t_dq, [&](int ks) { return dsb + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
+        mma_tmem_x_ones(t_aux, [&](int ks) { return dsb + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
+        ptx::mma_commit_elect(&kv_empty[st]);
+        ptx::mma_commit_elect(&ds_empty[db]);
+        ++nq;
+      } else if (ns < cnt && ptx::mbar_test(&kv_full[ns % NST], (ns / NST) & 1) &&
+                 ptx::mbar_test(&s_empty, (ns & 1) ^ 1)) {
+        const int k = ns, st = k % NST;
+        const uint8_t* sK = sKV + st * 2 * C::TILE;
+        ptx::tc_fence_after();
+        mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
+        mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
+        ptx::mma_commit_elect(&s_full);
+        ENTMAX_TRACE_K(3, 8 * k + 0);
+        ++ns;
+      } else {
+        __nanosleep(32);
+      }
     }
     ptx::mma_commit_elect(&acc_full);
   } else {
@@ -618,7 +627,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
             __nv_bfloat16* __restrict__ dv) {
   using C = Cfg<D>;
   constexpr bool ALIAS = (D == 128);
-  constexpr int NST = (D == 64) ? 3 : 2;
+  constexpr int NST = (D == 64) ? 5 : 2;   // Q/dO/τ/δ stages
   constexpr uint32_t STAGE = 2 * C::TILE + 1024;   // Q_i | dO_i | τ_i[128] | δ_i[128]
   constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dSᵀ is kDS·dSᵀ (exact doubling)
   extern __shared__ uint8_t smem_raw[];
@@ -684,33 +693,36 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
     }
   } else if (warp == 9) {
+    // Event-driven issue: dV/dK(k) as soon as Pᵀ/dSᵀ(k) are written, else Sᵀ/dPᵀ of the next tile once
+    // its Q/dO/τ/δ stage has landed and the previous Sᵀ/dPᵀ are read (d = 64) — or, with Pᵀ/dSᵀ aliased
+    // onto them (d = 128), once dV/dK of the previous tile are issued (the in-order pipe orders them)
     ptx::mbar_wait(&bar_kv, 0);
-    auto issue_sdp = [&](int k) {
-      const int st = k % NST;
-      const uint8_t* stg = sStage + st * STAGE;
-      ptx::mbar_wait(&qd_full[st], (k / NST) & 1);
-      ENTMAX_TRACE_K(2, 4096 + k);
-      if (!ALIAS) ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
-      ENTMAX_TRACE_K(2, 4160 + k);
-      ptx::tc_fence_after();
-      mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
-      mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
-      ptx::mma_commit_elect(&s_full);
-      ENTMAX_TRACE_K(2, 8 * k + 0);
-    };
-    if (cnt > 0) issue_sdp(0);
-    for (int k = 0; k < cnt; ++k) {
-      if (!ALIAS && k + 1 < cnt) issue_sdp(k + 1);
-      const int st = k % NST;
-      const uint8_t* stg = sStage + st * STAGE;
-      ptx::mbar_wait(&p_full, k & 1);
-      ENTMAX_TRACE_K(2, 8 * k + 1);
-      ptx::tc_fence_after();
-      mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
-      mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
-      ptx::mma_commit_elect(&qd_empty[st]);
-      if (!ALIAS) ptx::mma_commit_elect(&p_empty);   // (aliased Pᵀ/dSᵀ: the next Sᵀ MMA orders it)
-      if (ALIAS && k + 1 < cnt) issue_sdp(k + 1);
+    int ns = 0, nv = 0;
+    while (nv < cnt) {
+      if (nv < ns && ptx::mbar_test(&p_full, nv & 1)) {
+        const int k = nv, st = k % NST;
+        const uint8_t* stg = sStage + st * STAGE;
+        ENTMAX_TRACE_K(2, 8 * k + 1);
+        ptx::tc_fence_after();
+        mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
+        mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
+        ptx::mma_commit_elect(&qd_empty[st]);
+        if (!ALIAS) ptx::mma_commit_elect(&p_empty);
+        ++nv;
+      } else if (ns < cnt && (ALIAS ? ns <= nv : ptx::mbar_test(&s_empty, (ns & 1) ^ 1)) &&
+                 ptx::mbar_test(&qd_full[ns % NST], (ns / NST) & 1)) {
+        const int k = ns, st = k % NST;
+        const uint8_t* stg = sStage + st * STAGE;
+        ENTMAX_TRACE_K(2, 4096 + k);
+        ptx::tc_fence_after();
+        mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
+        mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
+        ptx::mma_commit_elect(&s_full);
+        ENTMAX_TRACE_K(2, 8 * k + 0);
+        ++ns;
+      } else {
+        __nanosleep(32);
+      }
     }
     ptx::mma_commit_elect(&acc_full);
     ENTMAX_TRACE_K(2, 8001);
