@@ -236,33 +236,27 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 #endif
     }
   } else if (warp == 9) {
-    // Event-driven issue (two independent streams, one thread of control): P·V/U·V of the oldest tile
-    // whose P/U are written, else S of the next tile once its K/V stage has landed and its S buffer's
-    // previous P/U are consumed (S(k) is issued after PV(k − NSB) in program order; the in-order tensor
-    // pipe then never overwrites unread P/U).  A late TMA stage never holds up the P·V of ready tiles.
     ptx::mbar_wait(&bar_q, 0);
-    int ns = 0, npv = 0;
-    while (npv < ncand) {
-      if (npv < ns && ptx::mbar_test(&p_full[npv % NSB], (npv / NSB) & 1)) {
-        const int k = npv, st = k % NST, sb = k % NSB;
-        ENTMAX_TRACE_K(1, 8 * k + 1);
-        ptx::tc_fence_after();
-        const uint32_t buf = tmem + sb * 128;
-        const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
-        mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
-        if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
-        ptx::mma_commit_elect(&kv_empty[st]);
-        ++npv;
-      } else if (ns < ncand && ns < npv + NSB && ptx::mbar_test(&kv_full[ns % NST], (ns / NST) & 1)) {
-        const int k = ns, st = k % NST;
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(tmem + (k % NSB) * 128, sQ, sKV + st * 2 * C::TILE, false);
-        ptx::mma_commit_elect(&s_full[k % NSB]);
-        ENTMAX_TRACE_K(1, 8 * k + 0);
-        ++ns;
-      } else {
-        __nanosleep(32);   // yield the SMSP's issue slots to the math warps while nothing is ready
-      }
+    auto issue_s = [&](int k) {
+      const int st = k % NST;
+      ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
+      ptx::tc_fence_after();
+      mma_rows_x_rows<D>(tmem + (k % NSB) * 128, sQ, sKV + st * 2 * C::TILE, false);
+      ptx::mma_commit_elect(&s_full[k % NSB]);
+      ENTMAX_TRACE_K(1, 8 * k + 0);
+    };
+    for (int k = 0; k < NSB && k < ncand; ++k) issue_s(k);
+    for (int k = 0; k < ncand; ++k) {
+      const int st = k % NST, sb = k % NSB;
+      ptx::mbar_wait(&p_full[sb], (k / NSB) & 1);
+      ENTMAX_TRACE_K(1, 8 * k + 1);
+      ptx::tc_fence_after();
+      const uint32_t buf = tmem + sb * 128;
+      const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
+      mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+      if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+      ptx::mma_commit_elect(&kv_empty[st]);
+      if (k + NSB < ncand) issue_s(k + NSB);
     }
     ptx::mma_commit_elect(&o_full);
   } else {
@@ -468,34 +462,31 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
 #endif
     }
   } else if (warp == 9) {
-    // Event-driven issue: dQ(k) (+ ρ) as soon as dS(k) is written, else S/dP of the next tile once its
-    // K/V stage has landed and the math warps have read the previous S/dP (they read all of it first)
     ptx::mbar_wait(&bar_q, 0);
-    int ns = 0, nq = 0;
-    while (nq < cnt) {
-      if (nq < ns && ptx::mbar_test(&ds_full[nq % NDS], (nq / NDS) & 1)) {
-        const int k = nq, st = k % NST, db = k % NDS;
-        const uint32_t dsb = t_ds + 64 * db;
-        ENTMAX_TRACE_K(3, 8 * k + 1);
-        ptx::tc_fence_after();
-        mma_tmem_x_tile<D>(t_dq, [&](int ks) { return dsb + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
-        mma_tmem_x_ones(t_aux, [&](int ks) { return dsb + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
-        ptx::mma_commit_elect(&kv_empty[st]);
-        ptx::mma_commit_elect(&ds_empty[db]);
-        ++nq;
-      } else if (ns < cnt && ptx::mbar_test(&kv_full[ns % NST], (ns / NST) & 1) &&
-                 ptx::mbar_test(&s_empty, (ns & 1) ^ 1)) {
-        const int k = ns, st = k % NST;
-        const uint8_t* sK = sKV + st * 2 * C::TILE;
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
-        mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
-        ptx::mma_commit_elect(&s_full);
-        ENTMAX_TRACE_K(3, 8 * k + 0);
-        ++ns;
-      } else {
-        __nanosleep(32);
-      }
+    auto issue_sdp = [&](int k) {
+      const int st = k % NST;
+      const uint8_t* sK = sKV + st * 2 * C::TILE;
+      ptx::mbar_wait(&kv_full[st], (k / NST) & 1);
+      ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
+      ptx::tc_fence_after();
+      mma_rows_x_rows<D>(t_s, sQ, sK, false);              // S  = Q_i K_jᵀ
+      mma_rows_x_rows<D>(t_dp, sDO, sK + C::TILE, false);  // dP = dO_i V_jᵀ
+      ptx::mma_commit_elect(&s_full);
+      ENTMAX_TRACE_K(3, 8 * k + 0);
+    };
+    if (cnt > 0) issue_sdp(0);
+    for (int k = 0; k < cnt; ++k) {
+      if (k + 1 < cnt) issue_sdp(k + 1);
+      const int st = k % NST;
+      const int db = k % NDS;
+      const uint32_t dsb = t_ds + 64 * db;
+      ptx::mbar_wait(&ds_full[db], (k / NDS) & 1);
+      ENTMAX_TRACE_K(3, 8 * k + 1);
+      ptx::tc_fence_after();
+      mma_tmem_x_tile<D>(t_dq, [&](int ks) { return dsb + 8 * ks; }, sKV + st * 2 * C::TILE, k > 0);
+      mma_tmem_x_ones(t_aux, [&](int ks) { return dsb + 8 * ks; }, sOnes, k > 0);   // ρ_i (r12)
+      ptx::mma_commit_elect(&kv_empty[st]);
+      ptx::mma_commit_elect(&ds_empty[db]);
     }
     ptx::mma_commit_elect(&acc_full);
   } else {
@@ -693,36 +684,33 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
     }
   } else if (warp == 9) {
-    // Event-driven issue: dV/dK(k) as soon as Pᵀ/dSᵀ(k) are written, else Sᵀ/dPᵀ of the next tile once
-    // its Q/dO/τ/δ stage has landed and the previous Sᵀ/dPᵀ are read (d = 64) — or, with Pᵀ/dSᵀ aliased
-    // onto them (d = 128), once dV/dK of the previous tile are issued (the in-order pipe orders them)
     ptx::mbar_wait(&bar_kv, 0);
-    int ns = 0, nv = 0;
-    while (nv < cnt) {
-      if (nv < ns && ptx::mbar_test(&p_full, nv & 1)) {
-        const int k = nv, st = k % NST;
-        const uint8_t* stg = sStage + st * STAGE;
-        ENTMAX_TRACE_K(2, 8 * k + 1);
-        ptx::tc_fence_after();
-        mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
-        mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
-        ptx::mma_commit_elect(&qd_empty[st]);
-        if (!ALIAS) ptx::mma_commit_elect(&p_empty);
-        ++nv;
-      } else if (ns < cnt && (ALIAS ? ns <= nv : ptx::mbar_test(&s_empty, (ns & 1) ^ 1)) &&
-                 ptx::mbar_test(&qd_full[ns % NST], (ns / NST) & 1)) {
-        const int k = ns, st = k % NST;
-        const uint8_t* stg = sStage + st * STAGE;
-        ENTMAX_TRACE_K(2, 4096 + k);
-        ptx::tc_fence_after();
-        mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
-        mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
-        ptx::mma_commit_elect(&s_full);
-        ENTMAX_TRACE_K(2, 8 * k + 0);
-        ++ns;
-      } else {
-        __nanosleep(32);
-      }
+    auto issue_sdp = [&](int k) {
+      const int st = k % NST;
+      const uint8_t* stg = sStage + st * STAGE;
+      ptx::mbar_wait(&qd_full[st], (k / NST) & 1);
+      ENTMAX_TRACE_K(2, 4096 + k);
+      if (!ALIAS) ptx::mbar_wait(&s_empty, (k & 1) ^ 1);
+      ENTMAX_TRACE_K(2, 4160 + k);
+      ptx::tc_fence_after();
+      mma_rows_x_rows<D>(t_s, sK, stg, false);             // Sᵀ  = K_j Q_iᵀ
+      mma_rows_x_rows<D>(t_dp, sV, stg + C::TILE, false);  // dPᵀ = V_j dO_iᵀ
+      ptx::mma_commit_elect(&s_full);
+      ENTMAX_TRACE_K(2, 8 * k + 0);
+    };
+    if (cnt > 0) issue_sdp(0);
+    for (int k = 0; k < cnt; ++k) {
+      if (!ALIAS && k + 1 < cnt) issue_sdp(k + 1);
+      const int st = k % NST;
+      const uint8_t* stg = sStage + st * STAGE;
+      ptx::mbar_wait(&p_full, k & 1);
+      ENTMAX_TRACE_K(2, 8 * k + 1);
+      ptx::tc_fence_after();
+      mma_tmem_x_tile<D>(t_dv, pt_col, stg + C::TILE, k > 0);   // dV += Pᵀ dO_i
+      mma_tmem_x_tile<D>(t_dk, dst_col, stg, k > 0);            // dK += dSᵀ Q_i
+      ptx::mma_commit_elect(&qd_empty[st]);
+      if (!ALIAS) ptx::mma_commit_elect(&p_empty);   // (aliased Pᵀ/dSᵀ: the next Sᵀ MMA orders it)
+      if (ALIAS && k + 1 < cnt) issue_sdp(k + 1);
     }
     ptx::mma_commit_elect(&acc_full);
     ENTMAX_TRACE_K(2, 8001);
