@@ -321,6 +321,9 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
           }
         }
       };
+#ifdef ENTMAX_FB_NOMATH   // diagnostics: pipeline time without the per-element math (results invalid)
+      if (tr == 12345.f)
+#endif
       if (masked) body(std::true_type{}); else body(std::false_type{});
       if constexpr ((E == 2 || E == 4) && !CU) su = fmul2(su, make_float2(0.5f, 0.5f));
       usum += su.x + su.y;
@@ -555,6 +558,9 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
             }
           }
         };
+#ifdef ENTMAX_FB_NOMATH
+        if (tr == 12345.f)
+#endif
         if (masked) body(std::true_type{}); else body(std::false_type{});
       }
       if (!seen) {   // (sign bits masked: U = 0 gives dS = ±0)
@@ -787,6 +793,9 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
             }
           }
         };
+#ifdef ENTMAX_FB_NOMATH
+        if (key == -12345)
+#endif
         if (!valid || diag) body(std::true_type{}); else body(std::false_type{});
       }
       if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 4);

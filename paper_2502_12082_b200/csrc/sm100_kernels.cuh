@@ -1,16 +1,12 @@
-// sm100_kernels.cuh — tcgen05 / TMEM / TMA kernels of the bf16 hot path (sm_100a).
+// sm100_kernels.cuh — shared pieces of the tcgen05 / TMEM / TMA kernels of the bf16 hot path (sm_100a).
 //
-// Every kernel is warp-specialised, one CTA per 128-row block of one head (B_r = B_c = 128):
-//   warps 0-3 : "math" warps — thread t owns TMEM lane t = row t of the S tile (a query row in
-//               the τ / output / dQ kernels, a key row in the dK/dV kernel) and runs the
-//               per-element α-entmax arithmetic in fp32 registers;
-//   warp  4   : TMA producer (lane 0 issues cp.async.bulk.tensor loads into a stage ring);
-//   warp  5   : MMA issuer (lane 0 issues tcgen05.mma, commits completions to mbarriers) and
-//               owner of the TMEM allocation.
-// Operand tiles are [128 rows × 64 bf16] boxes with the 128-byte swizzle; one such tile is
-// used K-major (contraction over d) or MN-major (contraction over rows) by descriptor choice.
-// P / U / dS tiles produced by the math warps are written to shared memory in the same
-// swizzled K-major layout and consumed by SS MMAs.
+// Every kernel is warp-specialised, one CTA per 128-row block of one head (B_r = B_c = 128): math
+// warps with thread ↔ TMEM lane ↔ row (a query row in the τ / output / dQ kernels, a key row in the
+// dK/dV kernel), one TMA producer warp (stage ring, mbarrier full/empty) and one MMA-issuer warp that
+// owns the TMEM allocation (see sm100_tau.cuh and sm100_fb.cuh for the per-kernel layouts).  Operand
+// tiles are [128 rows × 64 bf16] boxes with the 128-byte swizzle, used K-major (contraction over d) or
+// MN-major (contraction over rows) by descriptor choice; the operands the math warps produce (P, U,
+// dS) go back into TMEM and feed TS-MMAs.
 #pragma once
 
 #include <cuda.h>
@@ -22,8 +18,6 @@
 namespace entmax {
 namespace sm100 {
 
-constexpr int kThreads = 192;
-constexpr int kMathThreads = 128;
 constexpr uint32_t kChunkBytes = 128 * 128;   // one [128 rows × 64 bf16] SW128 box = 16 KB
 
 template <int D>
@@ -54,34 +48,6 @@ __device__ __forceinline__ void mma_rows_x_rows(uint32_t d_tmem, const uint8_t* 
     const uint32_t off = (ks >> 2) * kChunkBytes + (ks & 3) * 32;
     ptx::mma_bf16_ss_elect(d_tmem, ptx::sdesc_kmajor(sa + off), ptx::sdesc_kmajor(sb + off), idesc,
                      (accum_first || ks > 0) ? 1u : 0u);
-  }
-}
-
-// D[tmem, 128 × D] (+)= A·B, A = [128 × 128] K-major (thread-written P/U/dS tile, two 64-col
-// chunks), B = [128 rows × D] tile used MN-major (contraction over its 128 rows)
-template <int D>
-__device__ __forceinline__ void mma_p_x_tile(uint32_t d_tmem, const uint8_t* a, const uint8_t* b, bool accumulate) {
-  constexpr uint32_t idesc = ptx::idesc_bf16(128, D, 0, 1);
-  const uint32_t sa = ptx::smem_u32(a), sb = ptx::smem_u32(b);
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-    const uint32_t aoff = (ks >> 2) * kChunkBytes + (ks & 3) * 32;
-    const uint32_t boff = ks * 2048;
-    ptx::mma_bf16_ss_elect(d_tmem, ptx::sdesc_kmajor(sa + aoff), ptx::sdesc_mnmajor(sb + boff, kChunkBytes), idesc,
-                     (accumulate || ks > 0) ? 1u : 0u);
-  }
-}
-
-// write 32 fp32 values (columns c*32 .. c*32+31 of row r) as bf16 into a [128 × 128] K-major
-// SW128 tile (two 64-column chunks)
-__device__ __forceinline__ void st_row32_bf16(uint8_t* tile, int r, int c, const float* v) {
-  const uint32_t base = ptx::smem_u32(tile) + (c >> 1) * kChunkBytes;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t u = (c & 1) * 4 + q;
-    ptx::st_shared_v4(base + ptx::sw128_off(r, u), ptx::pack_bf16(v[8 * q + 0], v[8 * q + 1]),
-                      ptx::pack_bf16(v[8 * q + 2], v[8 * q + 3]), ptx::pack_bf16(v[8 * q + 4], v[8 * q + 5]),
-                      ptx::pack_bf16(v[8 * q + 6], v[8 * q + 7]));
   }
 }
 

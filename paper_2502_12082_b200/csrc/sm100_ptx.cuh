@@ -123,15 +123,6 @@ __device__ __forceinline__ void tma_load_4d_elect(void* dst, const CUtensorMap* 
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_4d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
-                                                 int c2, int c3, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, %4, "
-      "%5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
-      : "memory");
-}
-
 // 1-D bulk copy global → shared (16-byte aligned, size a multiple of 16) completing on `bar`, one elected lane
 __device__ __forceinline__ void bulk_load_elect(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -207,6 +198,61 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- CTA pairs (cta_group::2)
+// A 2-SM MMA (tcgen05.mma.cta_group::2, issued by the even CTA of a cluster pair) computes an M = 256 tile:
+// each CTA holds its own 128 rows of A and half of the N columns of B at the same shared-memory offsets,
+// and receives its 128 accumulator rows in its own TMEM.
+// TMA load into this CTA's shared memory whose complete_tx is counted on the barrier at cluster address
+// `bar_c` (normally the leader CTA's barrier, from mapa(…, 0)).
+__device__ __forceinline__ void tma_load_4d_2sm_elect(void* dst, const CUtensorMap* m, uint32_t bar_c, int c0, int c1,
+                                                      int c2, int c3) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_c), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// D[tmem] (+)= A[smem] · B[smem] over the CTA pair (kind::f16, cta_group::2, one elected thread of the leader)
+__device__ __forceinline__ void mma2_bf16_ss_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                   uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] · B[smem] over the CTA pair (A rows from each CTA's own TMEM)
+__device__ __forceinline__ void mma2_bf16_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                                   uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// completion of the pair's earlier MMAs → one arrive on the barrier at this offset in every CTA of `mask`
+__device__ __forceinline__ void mma2_commit_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// TMEM allocation of a CTA pair: the same warp of both CTAs allocates; both get the same column address
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t NCOLS>
+__device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
 }
 
 // generic-proxy smem writes → visible to the async proxy (tcgen05.mma operand reads)
@@ -374,34 +420,7 @@ __device__ __forceinline__ void st_shared_v4(uint32_t saddr, uint32_t a, uint32_
 }
 
 // scalar shared-memory accesses by 32-bit shared address (keeps the compiler on STS/LDS when the
-// pointer arithmetic would otherwise lose the address space); *_pred store only where p != 0
-__device__ __forceinline__ void st_shared_f32_pred(uint32_t saddr, float v, uint32_t p) {
-  asm volatile("{.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.f32 [%0], %1;\n\t}" ::"r"(saddr), "f"(v),
-               "r"(p) : "memory");
-}
-__device__ __forceinline__ void st_shared_u16_pred(uint32_t saddr, uint32_t v, uint32_t p) {
-  asm volatile("{.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n\t}" ::"r"(saddr),
-               "h"((unsigned short)v), "r"(p) : "memory");
-}
-__device__ __forceinline__ void st_shared_f2_pred(uint32_t saddr, float2 v, uint32_t p) {
-  asm volatile("{.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q st.shared.v2.f32 [%0], {%1, %2};\n\t}" ::"r"(saddr),
-               "f"(v.x), "f"(v.y), "r"(p) : "memory");
-}
-// list append: if v > thr, store v at [as] and the u16 tag at [aj], then advance as by 1024 and aj
-// by 512 (one predicate, no branch; the layout of the τ kernel's per-thread candidate lists)
-__device__ __forceinline__ void append_if_gt(uint32_t& as, uint32_t& aj, float v, float thr, uint32_t tag) {
-  asm volatile(
-      "{.reg .pred q;\n\tsetp.gt.f32 q, %2, %3;\n\t@q st.shared.f32 [%0], %2;\n\t@q st.shared.u16 [%1], %4;\n\t"
-      "@q add.u32 %0, %0, 1024;\n\t@q add.u32 %1, %1, 512;\n\t}"
-      : "+r"(as), "+r"(aj)
-      : "f"(v), "f"(thr), "h"((unsigned short)tag)
-      : "memory");
-}
-__device__ __forceinline__ float2 ld_shared_f2(uint32_t saddr) {
-  float2 v;
-  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(saddr) : "memory");
-  return v;
-}
+// pointer arithmetic would otherwise lose the address space)
 __device__ __forceinline__ void st_shared_f32(uint32_t saddr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(saddr), "f"(v) : "memory");
 }

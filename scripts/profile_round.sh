@@ -7,7 +7,7 @@ TAG=${1:-r01}
 O=gpurun_out
 mkdir -p $O
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-rowwise --no-sweep > $O/${TAG}_launches_bench.log 2>&1
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > $O/${TAG}_launches_bench.log 2>&1
 for K in tau_kernel out_kernel dkdv_kernel dq_kernel; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 -f \
       -o $O/${TAG}_full_$K python scripts/run_fwd.py gaussian 1.0 bwd > $O/${TAG}_full_$K.log 2>&1
