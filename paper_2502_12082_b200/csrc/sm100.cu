@@ -4,6 +4,7 @@
 #include "sm100_kernels.cuh"
 #include "sm100_tau.cuh"
 #include "sm100_fb.cuh"
+#include "sm100_fb2.cuh"
 #include "tmap.h"
 
 namespace entmax {
@@ -58,6 +59,33 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
       return fail(ENTMAX_ERR_CUDA, "tau_sm100 launch: %s", cudaGetErrorString(e));
   }
   if (int rc = cuda_status("tau_sm100")) return rc;
+#ifndef ENTMAX_OUT1   // diagnostics: the 1-SM output kernel at d = 128 too
+  // d = 128: output pass on CTA pairs (2-SM MMAs, sm100_fb2.cuh), measured 16 % faster at config 5
+  // (N = 32768 causal: 5.66 → 4.76 ms).  d = 64 keeps the 1-SM kernel: there a tile's MMAs take half as
+  // long and the pair's cross-CTA P handshake is no longer hidden (1.03 → 1.59 ms at config 2).
+  if constexpr (D == 128) {
+    // V halves as MN-major SW128 boxes (SW64 [128 × 32] boxes would serve d = 64)
+    CUtensorMap tvh;
+    const bool ok = D == 64 ? make_tmap_bhnd_sw64(&tvh, v, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn)
+                            : make_tmap_bhnd(&tvh, v, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn);
+    if (!ok) return fail(ENTMAX_ERR_INVALID_ARG, "cuTensorMapEncodeTiled failed (V halves)");
+    const size_t sm2 = Out2Cfg<D>::smem(g.Tc);
+    const dim3 grid2((g.Tr + 1) & ~1, g.B * g.H);
+    ProfScope ps("out_sm100", st);
+    cudaError_t e;
+    if (o2 != nullptr) {
+      if (int rc = set_smem(out2_kernel<D, E, true, CU>, sm2)) return rc;
+      e = launch_pdl(out2_kernel<D, E, true, CU>, grid2, dim3(kFbThreads), sm2, st, tq, tk64, tvh, g, ap, tau, cand_cnt,
+                     cand_idx, (__nv_bfloat16*)o, (float*)o2, mask, row_cnt, row_idx);
+    } else {
+      if (int rc = set_smem(out2_kernel<D, E, false, CU>, sm2)) return rc;
+      e = launch_pdl(out2_kernel<D, E, false, CU>, grid2, dim3(kFbThreads), sm2, st, tq, tk64, tvh, g, ap, tau, cand_cnt,
+                     cand_idx, (__nv_bfloat16*)o, (float*)nullptr, mask, row_cnt, row_idx);
+    }
+    if (e != cudaSuccess) return fail(ENTMAX_ERR_CUDA, "out_sm100 launch: %s", cudaGetErrorString(e));
+    return cuda_status("out_sm100");
+  }
+#endif
   const size_t sm = out_smem<D>(g.Tc);
   if (o2 != nullptr) {
     if (int rc = set_smem(out_kernel<D, E, true, CU>, sm)) return rc;

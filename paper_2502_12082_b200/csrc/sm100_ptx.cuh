@@ -394,6 +394,18 @@ __device__ __forceinline__ uint64_t sdesc_mnmajor(uint32_t saddr, uint32_t chunk
   return sdesc_sw128(saddr, chunk_bytes, 1024);
 }
 
+// MN-major operand with the 64-byte swizzle: 32-element MN rows of 64 B per K row, 8 K rows per 512-B atom;
+// K-step of 16 rows = +1024 B (layout type 4).
+__device__ __forceinline__ uint64_t sdesc_mnmajor_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;                       // LBO (one MN atom: unused)
+  d |= (uint64_t)((512u >> 4) & 0x3FFFu) << 32;  // SBO: next 8 K rows
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
 // kind::f16 instruction descriptor: D fp32, A/B bf16, M, N, majors (0 = K-major, 1 = MN-major).
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn) {
   return (1u << 4)            // D format: f32

@@ -40,4 +40,20 @@ inline bool make_tmap_bhnd(CUtensorMap* m, const void* base, int B, int H, int N
   return r == CUDA_SUCCESS;
 }
 
+// Same tensor, box {box_cols elements of d, box_rows rows} with the 64-byte swizzle (box_cols = 32): the
+// MN-major SW64 layout of a [rows × 32] operand (each CTA's d-half of V at d = 64 in the 2-SM kernels).
+inline bool make_tmap_bhnd_sw64(CUtensorMap* m, const void* base, int B, int H, int N, int d, long long sb,
+                                long long sh, long long sn, int box_rows = 128) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)N, (cuuint64_t)H, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)sn * 2, (cuuint64_t)sh * 2, (cuuint64_t)sb * 2};
+  cuuint32_t box[4] = {32, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace entmax

@@ -14,9 +14,11 @@ MODES = {0: ("c1 SS 128x128x64", 2 * 128 * 128 * 64), 1: ("c1 SS 128x256x64", 2 
          2: ("c1 TS 128x64x128", 2 * 128 * 64 * 128), 3: ("c1 SS 128x64x128", 2 * 128 * 64 * 128),
          4: ("c2 SS 256x128x64", 2 * 128 * 128 * 64), 5: ("c2 SS 256x256x64", 2 * 128 * 256 * 64),
          6: ("c2 TS 256x128x128", 2 * 128 * 128 * 128), 7: ("c1 TS 128x128x128", 2 * 128 * 128 * 128),
-         8: ("c1 TS 128x256x128", 2 * 128 * 256 * 128)}
+         9: ("c2 TS 256x64x128 SW64", 2 * 128 * 64 * 128), 10: ("c2 SS 256x64x128 SW64", 2 * 128 * 64 * 128)}
 out = {}
 for mode, (name, fl) in MODES.items():
+    if len(sys.argv) > 2 and str(mode) not in sys.argv[2].split(','):
+        continue
     for grid in (2, 148):
         cyc = torch.zeros(grid, dtype=torch.int64, device="cuda")
         ms = ctypes.c_float()

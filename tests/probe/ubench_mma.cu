@@ -11,6 +11,8 @@
 //   mode 6: cta_group::2 TS  M256 N128 K128  (8 instr)   B MN-major, 64 N-columns per CTA
 //   mode 7: cta_group::1 TS  M128 N128 K128  (8 instr)
 //   mode 8: cta_group::1 TS  M128 N256 K128  (8 instr)
+//   mode 9: cta_group::2 TS  M256 N64  K128  (8 instr)   B MN-major SW64, 32 N-columns per CTA (P·V at d = 64)
+//   mode 10: cta_group::2 SS M256 N64  K128  (8 instr)   A K-major SW128, B MN-major SW64
 #include <cuda_bf16.h>
 #include <cstdio>
 
@@ -45,7 +47,7 @@ __device__ __forceinline__ void commit2_mc(uint64_t* bar, uint16_t mask) {
 
 template <int MODE>
 struct M {
-  static constexpr bool pair = MODE == 4 || MODE == 5 || MODE == 6;
+  static constexpr bool pair = MODE == 4 || MODE == 5 || MODE == 6 || MODE == 9 || MODE == 10;
 };
 
 template <int MODE>
@@ -96,6 +98,17 @@ __device__ __forceinline__ void tile(uint32_t tmem, uint32_t sa, uint32_t sb, in
     for (int ks = 0; ks < 8; ++ks)
       ptx::mma_bf16_ts_elect(tmem + (t & 1) * 128, tmem + 256 + ks * 8, ptx::sdesc_mnmajor(sb + ks * 2048, CH), id,
                              ks > 0);
+  } else if constexpr (MODE == 9) {
+    constexpr uint32_t id = ptx::idesc_bf16(256, 64, 0, 1);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+      mma2_ts(tmem + (t & 1) * 64, tmem + 256 + ks * 8, ptx::sdesc_mnmajor_sw64(sb + ks * 1024), id, ks > 0);
+  } else if constexpr (MODE == 10) {
+    constexpr uint32_t id = ptx::idesc_bf16(256, 64, 0, 1);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+      mma2_ss(tmem + (t & 1) * 64, ptx::sdesc_kmajor(sa + (ks >> 2) * CH + (ks & 3) * 32),
+              ptx::sdesc_mnmajor_sw64(sb + ks * 1024), id, ks > 0);
   } else if constexpr (MODE == 8) {
     constexpr uint32_t id = ptx::idesc_bf16(128, 256, 0, 1);
 #pragma unroll
@@ -194,6 +207,8 @@ extern "C" int mma_rate_run(int mode, int grid, int ntile, long long* cycles, fl
     case 6: return run<6>(grid, ntile, cycles, ms);
     case 7: return run<7>(grid, ntile, cycles, ms);
     case 8: return run<8>(grid, ntile, cycles, ms);
+    case 9: return run<9>(grid, ntile, cycles, ms);
+    case 10: return run<10>(grid, ntile, cycles, ms);
   }
   return 1;
 }
