@@ -440,6 +440,8 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       for (int c = 0; c < kCapQ; ++c) above += ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u) > thr ? 1 : 0;
       atomicOr(&s_overflow, above * list_len() > kCapQ * kCapQ ? 3 : 1);
     }
+    int* qcnt = reinterpret_cast<int*>(xch) + kTauMath;   // [4][128] list lengths (xch[0..511]: row maxima)
+    qcnt[qc * kBr + r] = list_len();
     bool fallback = pair_any(0);
     if (tid == 0 && s_fallback == 1) ENTMAX_TRACE_COUNT(8100);
     if (tid == 0 && s_fallback == 2) ENTMAX_TRACE_COUNT(8103);
@@ -455,58 +457,84 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::named_bar_sync(1, kTauMath);
       stream_pass(false);
       if (list_len() > kCapQ) s_overflow = 1;
+      qcnt[qc * kBr + r] = list_len();
       fallback = pair_any(1);
       if (tid == 0 && fallback) ENTMAX_TRACE_COUNT(8101);
     }
 
     if (!fallback) {
       // ---- T iterations of Alg. 1 on the row lists: fixed-point sums (FxSum), so τ is bitwise
-      // reproducible whichever path produced the lists.
+      // reproducible whichever path produced the lists.  The four quarter lists of a row are summed by
+      // four adjacent lanes of one warp (thread → row 8·warp + lane/4, quarter lane % 4), so the row sums
+      // are two xor-shuffles per iteration — no block barriers in the iteration loop.
       if (tid == 0) ENTMAX_TRACE_EV(8005);
-      const int n = list_len();
+      const int rr = warp * 8 + (lane >> 2), qq = lane & 3;
+      const int rowr = i * kBr + rr;
+      const bool validr = rowr < g.N;
+      const uint32_t ls0r = ptx::smem_u32(list_s) + (uint32_t)(qq * kCapQ) * 512u + rr * 4;
+      const uint32_t lj0r = ptx::smem_u32(list_j) + (uint32_t)(qq * kCapQ) * 256u + rr * 2;
+      const int n = qcnt[qq * kBr + rr];
+      const float smr = fmax3(fmaxf(xch[rr], xch[128 + rr]), xch[256 + rr], xch[384 + rr]);
+      RowState rq = bracket_init(smr * ap.cp, g.causal ? (float)(rowr + 1) : (float)g.N, ap.alpha);
       // the first kReg entries live in registers for all T iterations (−∞ pads contribute zeros)
       constexpr int kReg = 12;
       float lr[kReg];
 #pragma unroll
-      for (int c = 0; c < kReg; ++c) lr[c] = c < n ? ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u) : -INFINITY;
+      for (int c = 0; c < kReg; ++c) lr[c] = c < n ? ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u) : -INFINITY;
       for (int t = 0; t < n_iter; ++t) {
-        FxSum q{0ull, 0ull, 0ull};
-        if constexpr (E != 0) {   // <= kCapQ (< 256) terms per thread: 32-bit partials
+        float a0, a1, a2;
+        if constexpr (E != 0) {   // <= 4·kCapQ (< 256) terms per row: 32-bit fixed-point sums
           uint32_t p0 = 0, p1 = 0, p2 = 0;
 #pragma unroll
-          for (int c = 0; c < kReg; ++c) accum_fx32<E>(fmaf(lr[c], ap.cp, -rs.tau), ap, p0, p1, p2);
+          for (int c = 0; c < kReg; ++c) accum_fx32<E>(fmaf(lr[c], ap.cp, -rq.tau), ap, p0, p1, p2);
 #pragma unroll 4
           for (int c = kReg; c < n; ++c)
-            accum_fx32<E>(fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau), ap, p0, p1, p2);
-          q = FxSum{p0, p1, p2};
+            accum_fx32<E>(fmaf(ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u), ap.cp, -rq.tau), ap, p0, p1, p2);
+#pragma unroll
+          for (int o = 1; o <= 2; o <<= 1) {
+            p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+            p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+            p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+          }
+          a0 = (float)p0 * (1.0f / u01);
+          a1 = (float)p1 * (1.0f / u01);
+          a2 = (float)p2 * (1.0f / u2);
         } else {
+          FxSum q{0ull, 0ull, 0ull};
 #pragma unroll
           for (int c = 0; c < kReg; ++c) {
-            const float x = fmaf(lr[c], ap.cp, -rs.tau);
+            const float x = fmaf(lr[c], ap.cp, -rq.tau);
             if (x > 0.f) accum_fx<E>(x, ap, u2, q);
           }
 #pragma unroll 4
           for (int c = kReg; c < n; ++c) {
-            const float x = fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau);
+            const float x = fmaf(ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u), ap.cp, -rq.tau);
             if (x > 0.f) accum_fx<E>(x, ap, u2, q);
           }
+#pragma unroll
+          for (int o = 1; o <= 2; o <<= 1) {
+            q.q0 += __shfl_xor_sync(0xffffffffu, q.q0, o);
+            q.q1 += __shfl_xor_sync(0xffffffffu, q.q1, o);
+            q.q2 += __shfl_xor_sync(0xffffffffu, q.q2, o);
+          }
+          a0 = (float)q.q0 * (1.0f / u01);
+          a1 = (float)q.q1 * (1.0f / u01);
+          a2 = (float)q.q2 * (1.0f / u2);
         }
-        float a0, a1, a2;
-        row_sum3_fx(q, a0, a1, a2);
-        alg1_update(rs, a0, a1, a2, ap);
+        alg1_update(rq, a0, a1, a2, ap);
       }
       if (tid == 0) ENTMAX_TRACE_EV(8008);
-      if (valid) {
-        if (qc == 0) tau_out[(long long)bh * g.N + row] = rs.tau;
+      if (validr) {
+        if (qq == 0) tau_out[(long long)bh * g.N + rowr] = rq.tau;
         // exact block activity from the final τ (same fma test as the output kernel)
         const uint32_t af = ptx::smem_u32(aflag);
 #pragma unroll
         for (int c = 0; c < kReg; ++c)
-          if (fmaf(lr[c], ap.cp, -rs.tau) > 0.f) ptx::st_shared_u8(af + ptx::ld_shared_u16(lj0 + (uint32_t)c * 256u), 1);
+          if (fmaf(lr[c], ap.cp, -rq.tau) > 0.f) ptx::st_shared_u8(af + ptx::ld_shared_u16(lj0r + (uint32_t)c * 256u), 1);
 #pragma unroll 4
         for (int c = kReg; c < n; ++c)
-          if (fmaf(ptx::ld_shared_f32(ls0 + (uint32_t)c * 512u), ap.cp, -rs.tau) > 0.f)
-            ptx::st_shared_u8(af + ptx::ld_shared_u16(lj0 + (uint32_t)c * 256u), 1);
+          if (fmaf(ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u), ap.cp, -rq.tau) > 0.f)
+            ptx::st_shared_u8(af + ptx::ld_shared_u16(lj0r + (uint32_t)c * 256u), 1);
       }
       if (tid == 0) ENTMAX_TRACE_EV(8009);
       ptx::named_bar_sync(1, kTauMath);
