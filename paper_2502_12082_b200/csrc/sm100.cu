@@ -54,8 +54,8 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
     const size_t sm = TauSmem<D>::bytes(g.Tc);
     if (int rc = set_smem(tau_kernel<D, E>, sm)) return rc;
     ProfScope ps("tau_sm100", st);
-    if (cudaError_t e = launch_pdl(tau_kernel<D, E>, dim3((g.Tr + 1) & ~1, g.B * g.H), dim3(kTauThreads), sm, st, tq,
-                                   tk64, g, ap, n_iter, tau, cand_cnt, cand_idx))
+    if (cudaError_t e = launch_pdl(tau_kernel<D, E>, dim3(g.Tr, g.B * g.H), dim3(kTauThreads), sm, st, tq,
+                                   tk, g, ap, n_iter, tau, cand_cnt, cand_idx))
       return fail(ENTMAX_ERR_CUDA, "tau_sm100 launch: %s", cudaGetErrorString(e));
   }
   if (int rc = cuda_status("tau_sm100")) return rc;

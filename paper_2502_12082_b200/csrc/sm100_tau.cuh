@@ -116,14 +116,11 @@ struct TauSmem {
   static size_t bytes(int Tc) { return fixed + 2 * (size_t)Tc + 64; }   // cflag, aflag (u8)
 };
 
-// Launched as clusters of two CTAs = two adjacent query blocks of the same head, which stream the
-// same K blocks: each CTA TMA-loads half of every K tile (64 rows) with .multicast::cluster, so an SM
-// issues 8 KB per tile instead of 16 KB (TMA issue on the SM is what slows the tensor pipe down,
-// see DESIGN.md §6).  MMA completions are committed to the empty barriers of both CTAs.
-// `tk` is a tensor map with 64-row boxes.  Grid x is rounded up to even; a CTA past T_r streams and
-// computes but writes nothing.
+// One CTA per 128-row query block, no cluster: the K tiles stream by plain TMA into a private ring (a
+// 2-CTA cluster sharing every K tile by multicast measured 4-11 % slower: the pair's stage reuse waits
+// for the slower CTA).  `tk` is a tensor map with 128-row boxes.
 template <int D, int E>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTauThreads, 1)
+__global__ void __launch_bounds__(kTauThreads, 1)
 tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk, Geom g, AlphaParams ap,
            int n_iter, float* __restrict__ tau_out, int32_t* __restrict__ cand_cnt, int32_t* __restrict__ cand_idx) {
   using C = Cfg<D>;
@@ -142,17 +139,15 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   int* rowcnt = reinterpret_cast<int*>(mshare + kBr);                        // [128] (spare)
   uint8_t* cflag = reinterpret_cast<uint8_t*>(rowcnt + kBr);                 // [Tc] candidate blocks (τ_lo)
   uint8_t* aflag = cflag + g.Tc;                                             // [Tc] exact active blocks
-  __shared__ __align__(8) uint64_t bar_q, k_full[NST], k_empty[NST], s_full[kTauSBuf], s_empty[kTauSBuf], dec_bar,
-      x_bar;
+  __shared__ __align__(8) uint64_t bar_q, k_full[NST], k_empty[NST], s_full[kTauSBuf], s_empty[kTauSBuf], dec_bar;
   __shared__ uint32_t tmem_base_sh;
-  __shared__ int s_fallback, s_overflow, s_peer_overflow[2];
+  __shared__ int s_fallback, s_overflow;
 
   const int i = blockIdx.x, bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
+  const int nkb = g.visible_kblocks(i);
   const bool real_cta = i < g.Tr;
-  const int nkb = g.visible_kblocks(min((i | 1), g.Tr - 1));   // identical for both CTAs of the pair
   const long long li = (long long)bh * g.Tr + i;
   // warm-up: the first W blocks only raise the running max and are streamed again at the end
 #ifndef ENTMAX_TAU_WDIV
@@ -166,14 +161,13 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     ptx::mbar_init(&bar_q, 1);
     for (int s = 0; s < NST; ++s) {
       ptx::mbar_init(&k_full[s], 1);
-      ptx::mbar_init(&k_empty[s], 2);      // one MMA commit from each CTA of the pair
+      ptx::mbar_init(&k_empty[s], 1);
     }
     for (int s = 0; s < kTauSBuf; ++s) {
       ptx::mbar_init(&s_full[s], 1);
       ptx::mbar_init(&s_empty[s], kTauMathWarps / kTauSBuf);   // the 4 warps of one group
     }
     ptx::mbar_init(&dec_bar, 1);
-    ptx::mbar_init(&x_bar, 1);
     ptx::fence_mbar_init();
     s_overflow = 0;
   }
@@ -185,7 +179,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   if (threadIdx.x == 0) ENTMAX_TRACE_EV(8000);
   if (warp == kTauMathWarps + 1) ptx::tmem_alloc<128 * kTauSBuf>(&tmem_base_sh);
   ptx::tc_fence_before();
-  ptx::cluster_sync();   // both CTAs' barriers exist before any multicast targets them
+  __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   ptx::griddep_launch_dependents();
@@ -203,10 +197,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::mbar_wait(&k_empty[st], ((k / NST) & 1) ^ 1);
       ENTMAX_TRACE_EV(6144 + k);
       ptx::mbar_arrive_expect_tx_elect(&k_full[st], C::TILE);   // both halves land here
-#pragma unroll
-      for (int c = 0; c < C::KCH; ++c)
-        ptx::tma_load_4d_mc_elect(sK + st * C::TILE + c * kChunkBytes + rank * (kChunkBytes / 2), &tk, &k_full[st],
-                                  c * 64, j * kBc + (int)rank * 64, h, b, 0x3);
+      tma_tile<D>(sK + st * C::TILE, &tk, &k_full[st], j * kBc, h, b);
       ++k;
     };
     for (int t = 0; t < nkb + W; ++t) load(t < nkb ? t : t - nkb);
@@ -233,7 +224,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ENTMAX_TRACE_EV(4 * k + 2);
       ptx::tc_fence_after();
       mma_rows_x_rows<D>(tmem + sb * 128, sQ, sK + st * C::TILE, false);
-      ptx::mma_commit_mc_elect(&k_empty[st], 0x3);
+      ptx::mma_commit_elect(&k_empty[st]);
       ptx::mma_commit_elect(&s_full[sb]);
       ++k;
     };
@@ -298,18 +289,13 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     // first step t >= 0 of a pass starting at global index k0 that belongs to this group
     auto first_t = [&](int k0) { return (qc - k0 % kTauSBuf + kTauSBuf) % kTauSBuf; };
 
-    // the two CTAs of the pair stream the same K blocks, so every fallback decision is joint
-    // (s_overflow is read after the barrier: every thread's write to it must be visible)
-    auto pair_any = [&](int use) {
+    // fallback decision of the CTA (s_overflow is read after the barrier: every thread's write to it must
+    // be visible): 0 lists complete; 1 rebuild them with the exact threshold (tier 1); 2 stream Alg. 3
+    // passes (tier 2) — taken directly when a list is more than twice over its capacity
+    auto decide = [&](int use) {
       ptx::named_bar_sync(1, kTauMath);
       if (tid == 0) {
-        const int flag = s_overflow;
-        ptx::st_cluster_u32(ptx::mapa(ptx::smem_u32(&s_peer_overflow[use]), peer), (uint32_t)flag);
-        ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&x_bar), peer));
-        ptx::mbar_wait_cluster(&x_bar, use);
-        // 0: lists complete; 1: rebuild them with the exact threshold (tier 1); 2: stream Alg. 3
-        // passes (tier 2) — taken directly when a list is more than twice over its capacity
-        const int any = flag | s_peer_overflow[use];
+        const int any = s_overflow;
         s_fallback = any == 0 ? 0 : (use == 1 || (any & 2)) ? 2 : 1;
       }
       ptx::named_bar_sync(1, kTauMath);
@@ -442,7 +428,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
     int* qcnt = reinterpret_cast<int*>(xch) + kTauMath;   // [4][128] list lengths (xch[0..511]: row maxima)
     qcnt[qc * kBr + r] = list_len();
-    bool fallback = pair_any(0);
+    bool fallback = decide(0);
     if (tid == 0 && s_fallback == 1) ENTMAX_TRACE_COUNT(8100);
     if (tid == 0 && s_fallback == 2) ENTMAX_TRACE_COUNT(8103);
     if (tid == 0) ENTMAX_TRACE_COUNT(8102);
@@ -458,7 +444,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       stream_pass(false);
       if (list_len() > kCapQ) s_overflow = 1;
       qcnt[qc * kBr + r] = list_len();
-      fallback = pair_any(1);
+      fallback = decide(1);
       if (tid == 0 && fallback) ENTMAX_TRACE_COUNT(8101);
     }
 
@@ -549,8 +535,8 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
         ptx::mbar_arrive(&dec_bar);
       }
     } else {
-      // ---- tier 2: streaming Alg. 3 passes over every visible block (the pair streams the same
-      // blocks, so no per-CTA pruning); the output kernel gets this CTA's τ_lo candidate blocks
+      // ---- tier 2: streaming Alg. 3 passes over every visible block; the output kernel gets this CTA's
+      // τ_lo candidate blocks
       if (warp == 0) {
         if (real_cta) {
           const int nb = compact_flags(cflag, nkb, cand_idx + li * g.Tc);
@@ -600,7 +586,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   }
   ptx::tc_fence_before();
   if (threadIdx.x == 0) ENTMAX_TRACE_EV(8006);
-  ptx::cluster_sync();   // no CTA leaves while its peer may still multicast into it
+  __syncthreads();
   if (threadIdx.x == 0) ENTMAX_TRACE_EV(8007);
   if (warp == kTauMathWarps + 1) ptx::tmem_dealloc<128 * kTauSBuf>(tmem);
 }
