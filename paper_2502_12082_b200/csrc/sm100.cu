@@ -24,6 +24,10 @@ constexpr size_t dq_smem() {
   return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 5 : 2) * 2 * Cfg<D>::TILE + kOnesBytes;
 }
 
+#ifndef ENTMAX_DKDV_MW
+#define ENTMAX_DKDV_MW 16   // math warps of the dK/dV kernel
+#endif
+
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
 
 template <typename K>
@@ -112,9 +116,10 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
   {
     const size_t sm = dkdv_smem<D>();
-    if (int rc = set_smem(dkdv_kernel<D, E, CU>, sm)) return rc;
+    constexpr int MW = ENTMAX_DKDV_MW;
+    if (int rc = set_smem(dkdv_kernel<D, E, CU, MW>, sm)) return rc;
     ProfScope ps("dkdv_sm100", st);
-    if (cudaError_t e = launch_pdl(dkdv_kernel<D, E, CU>, dim3(g.Tc, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo,
+    if (cudaError_t e = launch_pdl(dkdv_kernel<D, E, CU, MW>, dim3(g.Tc, g.B * g.H), dim3(dkdv_threads<MW>()), sm, st, tq, tk, tv, tdo,
                                    g, ap, td, col_cnt, col_idx, kbar, (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
       return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
   }

@@ -607,16 +607,49 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   if (warp == 9) ptx::tmem_dealloc<512>(tmem);
 }
 
+// Store NC fp32 TMEM columns of one row as bf16 × scale (16-column TMEM loads; warp-collective loads, only
+// lanes with do_store write).
+template <int NC>
+__device__ __forceinline__ void store_cols_bf16(uint32_t taddr, __nv_bfloat16* dst, float scale, bool zero,
+                                                bool do_store) {
+#pragma unroll 1
+  for (int c = 0; c < NC / 16; ++c) {
+    uint32_t r[16];
+    if (!zero) {
+      ptx::tmem_ld16(taddr + c * 16, r);
+      ptx::tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) r[e] = 0u;
+    }
+    if (!do_store) continue;
+    uint4* p = reinterpret_cast<uint4*>(dst + c * 16);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = ptx::pack_bf16(__uint_as_float(r[8 * q + 2 * e]) * scale, __uint_as_float(r[8 * q + 2 * e + 1]) * scale);
+      p[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
 // =====================================================================================
 // dK_j, dV_j over 𝒦_j (Alg. 4).  TMEM lanes = the 128 keys of block j.
 //   Sᵀ = K_j Q_iᵀ, dPᵀ = V_j dO_iᵀ (SS); Pᵀ and dSᵀ = Uᵀ ⊙ (dPᵀ − δ_i) to TMEM;
 //   dV_j += Pᵀ dO_i, dK_j += dSᵀ Q_i (TS); dK scaled by c at the end (Eq. 1).
+// MW math warps (8 or 16): warp w owns TMEM lanes 32·(w & 3) and the query-column slice w >> 2 of width
+// CW = 128·4/MW; MW = 16 gives four warps per scheduler to hide the per-element latency chains.
 // d = 64: Sᵀ [0,128) dPᵀ [128,256) Pᵀ [256,320) dSᵀ [320,384) dV [384,448) dK [448,512), so the
 //         next step's Sᵀ/dPᵀ overlap this step's math.
-// d = 128: Pᵀ/dSᵀ overwrite each warpgroup's own Sᵀ/dPᵀ columns (dV [256,384), dK [384,512)).
+// d = 128: Pᵀ/dSᵀ overwrite each slice's own Sᵀ/dPᵀ columns (dV [256,384), dK [384,512)).
 // =====================================================================================
-template <int D, int E, bool CU>
-__global__ void __launch_bounds__(kFbThreads, 1)
+template <int MW>
+constexpr int dkdv_threads() { return 32 * MW + 64; }
+
+template <int D, int E, bool CU, int MW>
+__global__ void __launch_bounds__(dkdv_threads<MW>(), 1)
 dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
             const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
             const float* __restrict__ td, const int32_t* __restrict__ col_cnt,
@@ -627,6 +660,13 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   constexpr int NST = (D == 64) ? 5 : 2;   // Q/dO/τ/δ stages
   constexpr uint32_t STAGE = 2 * C::TILE + 1024;   // Q_i | dO_i | τ_i[128] | δ_i[128]
   constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dSᵀ is kDS·dSᵀ (exact doubling)
+  constexpr int kMath = 32 * MW;
+  constexpr int SL = MW / 4;           // query-column slices
+  constexpr int CW = 128 / SL;         // query columns per thread
+  constexpr int NH = CW / 32;          // 32-column halves per thread
+  constexpr int WPR = CW / 2;          // bf16x2 words per thread of Pᵀ / dSᵀ
+  constexpr int KPS = CW / 16;         // MMA k-steps per slice
+  constexpr int PROD = MW, MMAW = MW + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sK = smem;
@@ -647,14 +687,14 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       ptx::mbar_init(&qd_empty[s], 1);
     }
     ptx::mbar_init(&s_full, 1);
-    ptx::mbar_init(&s_empty, 8);
-    ptx::mbar_init(&p_full, 8);
+    ptx::mbar_init(&s_empty, MW);
+    ptx::mbar_init(&p_full, MW);
     ptx::mbar_init(&p_empty, 1);
     ptx::mbar_init(&acc_full, 1);
     ptx::fence_mbar_init();
   }
   if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8002);
-  if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
+  if (warp == MMAW) ptx::tmem_alloc<512>(&tmem_base_sh);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -667,10 +707,15 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   const int cnt = dense ? g.Tr - i0 : col_cnt[lj];
   const BlockList list{dense ? nullptr : col_idx + lj * g.Tr, i0};
   const uint32_t t_dv = tmem + (ALIAS ? 256 : 384), t_dk = t_dv + D;
-  auto pt_col = [&](int ks) { return ALIAS ? t_s + 8 * ks + (ks >= 4 ? 32 : 0) : tmem + 256 + 8 * ks; };
-  auto dst_col = [&](int ks) { return ALIAS ? t_dp + 8 * ks + (ks >= 4 ? 32 : 0) : tmem + 320 + 8 * ks; };
+  // k-step ks (16 query columns = 8 TMEM words) of Pᵀ / dSᵀ: slice ks / KPS, word 8·(ks % KPS) of it
+  auto pt_col = [&](int ks) {
+    return ALIAS ? t_s + CW * (ks / KPS) + 8 * (ks % KPS) : tmem + 256 + 8 * ks;
+  };
+  auto dst_col = [&](int ks) {
+    return ALIAS ? t_dp + CW * (ks / KPS) + 8 * (ks % KPS) : tmem + 320 + 8 * ks;
+  };
 
-  if (warp == 8) {
+  if (warp == PROD) {
     ptx::tma_prefetch_desc(&tq);
     ptx::tma_prefetch_desc(&tdo);
     ptx::mbar_arrive_expect_tx_elect(&bar_kv, 2 * C::TILE);
@@ -689,7 +734,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       tma_tile<D>(stg, &tq, &qd_full[st], ib * kBr, h, b);
       tma_tile<D>(stg + C::TILE, &tdo, &qd_full[st], ib * kBr, h, b);
     }
-  } else if (warp == 9) {
+  } else if (warp == MMAW) {
     ptx::mbar_wait(&bar_kv, 0);
     auto issue_sdp = [&](int k) {
       const int st = k % NST;
@@ -728,29 +773,30 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
     for (int k = 0; k < cnt; ++k) {
       const int ib = list[k], st = k % NST;
       const uint8_t* stg = sStage + st * STAGE;
-      const uint32_t tq4 = ptx::smem_u32(stg + 2 * C::TILE) + wg * 256;   // τ_i (float4 units below)
-      const uint32_t dl4 = tq4 + 512;                                      // δ_i
+      const uint32_t tq4 = ptx::smem_u32(stg + 2 * C::TILE) + wg * (CW * 4);   // τ_i (float4 units below)
+      const uint32_t dl4 = tq4 + 512;                                        // δ_i
       const bool diag = g.causal && ib == j;   // queries below the key inside the diagonal block
       ptx::mbar_wait(&qd_full[st], (k / NST) & 1);   // τ_i, δ_i staged by the producer warp
       ptx::mbar_wait(&s_full, k & 1);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 3);
       ptx::tc_fence_after();
-      uint32_t pp[32], pd[32];
-      // all 64 columns of Sᵀ and dPᵀ are read at once, so the MMA warp can start Sᵀ/dPᵀ(k+1) while this
-      // warp still computes tile k (one wait instead of two; the buffers are free ~a TMEM latency in)
-      float sa[2][32], da[2][32];
-      ld32f_nowait(lane_base + t_s + wg * 64, sa[0]);
-      ld32f_nowait(lane_base + t_dp + wg * 64, da[0]);
-      ld32f_nowait(lane_base + t_s + wg * 64 + 32, sa[1]);
-      ld32f_nowait(lane_base + t_dp + wg * 64 + 32, da[1]);
+      uint32_t pp[WPR], pd[WPR];
+      // all of this thread's columns of Sᵀ and dPᵀ are read at once, so the MMA warp can start
+      // Sᵀ/dPᵀ(k+1) while this warp still computes tile k
+      float sa[NH][32], da[NH][32];
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        ld32f_nowait(lane_base + t_s + wg * CW + hh * 32, sa[hh]);
+        ld32f_nowait(lane_base + t_dp + wg * CW + hh * 32, da[hh]);
+      }
       ptx::tmem_wait_ld();
       if (!ALIAS) {
         ptx::tc_fence_before();
         warp_arrive(&s_empty);
       }
-      if (lane == 0) ENTMAX_TRACE_K(2, 4288 + 8 * k + warp);
+      if (lane == 0) ENTMAX_TRACE_K(2, 4288 + 8 * k + (warp & 7));
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 0; hh < NH; ++hh) {
         const float(&s)[32] = sa[hh];
         const float(&dp)[32] = da[hh];
         auto body = [&](auto masked_c) {
@@ -763,31 +809,32 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
               const float2 dq2 = e == 0 ? make_float2(-d4.x, -d4.y) : make_float2(-d4.z, -d4.w);
               float2 x = ffma2(make_float2(s[q4 * 4 + e], s[q4 * 4 + e + 1]), make_float2(ap.cp, ap.cp), tq2);
               if constexpr (decltype(masked_c)::value) {
-                const int ql = wg * 64 + hh * 32 + q4 * 4 + e;
+                const int ql = wg * CW + hh * 32 + q4 * 4 + e;
                 if (!valid || (diag && ql < r)) x.x = kMaskX;
                 if (!valid || (diag && ql + 1 < r)) x.y = kMaskX;
               }
               const float2 g2 = fadd2(make_float2(dp[q4 * 4 + e], dp[q4 * 4 + e + 1]), dq2);
+              const int w = hh * 16 + q4 * 2 + (e >> 1);
               if constexpr (E == 2 || E == 4) {
                 uint32_t pb, ub;
                 pu_packed<E>(x, pb, ub);
-                pp[hh * 16 + q4 * 2 + (e >> 1)] = pb;
+                pp[w] = pb;
                 if constexpr (CU) {   // Û (r9)
-                  pd[hh * 16 + q4 * 2 + (e >> 1)] = mul_bf16x2(ub, ptx::pack_bf16(g2.x, g2.y));
+                  pd[w] = mul_bf16x2(ub, ptx::pack_bf16(g2.x, g2.y));
                 } else {   // 2dSᵀ = (2u)·(dPᵀ − δ): exact doubling, no relu (see the dQ kernel)
                   const float2 bb = E == 2 ? x : fmul2(fmul2(x, fabs2(x)), fabs2(x));
                   const float2 ds2 = fmul2(fadd2(bb, fabs2(bb)), g2);
-                  pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds2.x, ds2.y);
+                  pd[w] = ptx::pack_bf16(ds2.x, ds2.y);
                 }
               } else {
                 float2 p, u;
                 p_and_u2<E>(x, ap, p, u);
-                pp[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(p.x, p.y);
+                pp[w] = ptx::pack_bf16(p.x, p.y);
                 if constexpr (CU)   // Û (r9)
-                  pd[hh * 16 + q4 * 2 + (e >> 1)] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
+                  pd[w] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
                 else {
                   const float2 ds = fmul2(u, g2);
-                  pd[hh * 16 + q4 * 2 + (e >> 1)] = ptx::pack_bf16(ds.x, ds.y);
+                  pd[w] = ptx::pack_bf16(ds.x, ds.y);
                 }
               }
             }
@@ -804,8 +851,13 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
         ptx::tc_fence_after();
       }
       if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 5);
-      ptx::tmem_st32(lane_base + pt_col(wg * 4), pp);
-      ptx::tmem_st32(lane_base + dst_col(wg * 4), pd);
+      if constexpr (WPR == 32) {
+        ptx::tmem_st32(lane_base + pt_col(wg * KPS), pp);
+        ptx::tmem_st32(lane_base + dst_col(wg * KPS), pd);
+      } else {
+        ptx::tmem_st16(lane_base + pt_col(wg * KPS), pp);
+        ptx::tmem_st16(lane_base + dst_col(wg * KPS), pd);
+      }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       warp_arrive(&p_full);
@@ -816,14 +868,15 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       ptx::mbar_wait(&acc_full, 0);
       ptx::tc_fence_after();
     }
-    const long long off = g.head_off(bh) + (long long)(valid ? key : 0) * g.sn + wg * (D / 2);
-    store_row_bf16<D / 2>(lane_base + t_dv + wg * (D / 2), dv + off, 1.0f, cnt == 0, valid);
-    store_row_bf16<D / 2>(lane_base + t_dk + wg * (D / 2), dk + off, ap.scale / kDS, cnt == 0, valid);
+    constexpr int DS = D / SL;   // dK / dV columns stored per thread
+    const long long off = g.head_off(bh) + (long long)(valid ? key : 0) * g.sn + wg * DS;
+    store_cols_bf16<DS>(lane_base + t_dv + wg * DS, dv + off, 1.0f, cnt == 0, valid);
+    store_cols_bf16<DS>(lane_base + t_dk + wg * DS, dk + off, ap.scale / kDS, cnt == 0, valid);
     if (kbar != nullptr) {
       // K̄_j = mean of the block's keys (fp32) for the dQ kernel's leak correction (reading r12), from the
       // K tile this CTA holds in shared memory (rows past N are TMA zero fill).  Thread → (16-byte unit u of
       // a row, row phase rp); partial sums reduced through the (now idle) stage buffers.
-      constexpr int UNITS = D / 8, RP = kFbMath / UNITS;
+      constexpr int UNITS = D / 8, RP = kMath / UNITS;
       ptx::mbar_wait(&bar_kv, 0);
       const int u = tid % UNITS, rp = tid / UNITS;
       const uint32_t kb0 = ptx::smem_u32(sK) + (uint32_t)(u >> 3) * kChunkBytes;
@@ -841,7 +894,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
       float* red = reinterpret_cast<float*>(sStage);   // [RP][D]
 #pragma unroll
       for (int e = 0; e < 8; ++e) red[rp * D + u * 8 + e] = a[e];
-      ptx::named_bar_sync(1, kFbMath);
+      ptx::named_bar_sync(1, kMath);
       if (tid < D) {
         float sum = 0.f;
         for (int p = 0; p < RP; ++p) sum += red[p * D + tid];
@@ -852,7 +905,7 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8003);
-  if (warp == 9) ptx::tmem_dealloc<512>(tmem);
+  if (warp == MMAW) ptx::tmem_dealloc<512>(tmem);
 }
 
 }  // namespace sm100
