@@ -24,8 +24,11 @@ constexpr size_t dq_smem() {
   return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 5 : 2) * 2 * Cfg<D>::TILE + kOnesBytes;
 }
 
+#ifndef ENTMAX_DQ_MW
+#define ENTMAX_DQ_MW 8      // math warps of the dQ kernel (16 measured slower: 1.075 -> 1.133 ms at config 2)
+#endif
 #ifndef ENTMAX_DKDV_MW
-#define ENTMAX_DKDV_MW 16   // math warps of the dK/dV kernel
+#define ENTMAX_DKDV_MW 16   // math warps of the dK/dV kernel (8: 1.64 ms, 16: 1.43 ms at config 2)
 #endif
 
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
@@ -126,9 +129,10 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
   if (int rc = cuda_status("dkdv_sm100")) return rc;
   {
     const size_t sm = dq_smem<D>();
-    if (int rc = set_smem(dq_kernel<D, E, CU>, sm)) return rc;
+    constexpr int MW = ENTMAX_DQ_MW;
+    if (int rc = set_smem(dq_kernel<D, E, CU, MW>, sm)) return rc;
     ProfScope ps("dq_sm100", st);
-    if (cudaError_t e = launch_pdl(dq_kernel<D, E, CU>, dim3(g.Tr, g.B * g.H), dim3(kFbThreads), sm, st, tq, tk, tv, tdo, g,
+    if (cudaError_t e = launch_pdl(dq_kernel<D, E, CU, MW>, dim3(g.Tr, g.B * g.H), dim3(dq_threads<MW>()), sm, st, tq, tk, tv, tdo, g,
                                    ap, tau, delta, row_cnt, row_idx, kbar, (__nv_bfloat16*)dq))
       return fail(ENTMAX_ERR_CUDA, "dq_sm100 launch: %s", cudaGetErrorString(e));
   }

@@ -117,25 +117,29 @@ __device__ __forceinline__ void store_row_bf16(uint32_t taddr, __nv_bfloat16* ds
   }
 }
 
-// dQ epilogue with the leak correction (reading r12): row ← c·(acc − ρ·K̄) for HALF fp32 columns, K̄ = kb[0..HALF)
-// (fp32, global), ρ this row's Σ_j dŜ_ij.
-template <int HALF>
+// dQ epilogue with the leak correction (reading r12): row ← c·(acc − ρ·K̄) for NC fp32 columns (16-column
+// TMEM loads), K̄ = kb[0..NC) (fp32, global), ρ this row's Σ_j dŜ_ij.
+template <int NC>
 __device__ __forceinline__ void store_row_bf16_corr(uint32_t taddr, __nv_bfloat16* dst, float scale, bool zero,
                                                     bool do_store, float rho, const float* __restrict__ kb) {
 #pragma unroll 1
-  for (int c = 0; c < HALF / 32; ++c) {
-    float v[32];
+  for (int c = 0; c < NC / 16; ++c) {
+    uint32_t r[16];
+    float v[16];
     if (!zero) {
-      ld_chunk(taddr + c * 32, v);
+      ptx::tmem_ld16(taddr + c * 16, r);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = __uint_as_float(r[e]);
     } else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[e] = 0.f;
+      for (int e = 0; e < 16; ++e) v[e] = 0.f;
     }
     if (!do_store) continue;
     if (kb != nullptr) {
-      const float4* k4 = reinterpret_cast<const float4*>(kb + c * 32);
+      const float4* k4 = reinterpret_cast<const float4*>(kb + c * 16);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < 4; ++q) {
         const float4 kk = __ldg(k4 + q);
         v[4 * q] = fmaf(-rho, kk.x, v[4 * q]);
         v[4 * q + 1] = fmaf(-rho, kk.y, v[4 * q + 1]);
@@ -143,9 +147,9 @@ __device__ __forceinline__ void store_row_bf16_corr(uint32_t taddr, __nv_bfloat1
         v[4 * q + 3] = fmaf(-rho, kk.w, v[4 * q + 3]);
       }
     }
-    uint4* p = reinterpret_cast<uint4*>(dst + c * 32);
+    uint4* p = reinterpret_cast<uint4*>(dst + c * 16);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 2; ++q)
       p[q] = make_uint4(ptx::pack_bf16(v[8 * q] * scale, v[8 * q + 1] * scale),
                         ptx::pack_bf16(v[8 * q + 2] * scale, v[8 * q + 3] * scale),
                         ptx::pack_bf16(v[8 * q + 4] * scale, v[8 * q + 5] * scale),
@@ -386,9 +390,14 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 // TMEM; dQ_i += dS K_j (TS-MMA); dQ scaled by c at the end (Eq. 1).
 // TMEM: S [0,128), dP [128,256), dS [256,320) (wg·32 + …), dQ [320, 320+D).
 // Issue order S,dP(k+1) | dQ(k): the next tile's scores are computed while the math warps form dS(k).
+// MW math warps (8 or 16): warp w owns TMEM lanes 32·(w & 3) and the key-column slice w >> 2 of width
+// CW = 128·4/MW.
 // =====================================================================================
-template <int D, int E, bool CU>
-__global__ void __launch_bounds__(kFbThreads, 1)
+template <int MW>
+constexpr int dq_threads() { return 32 * MW + 64; }
+
+template <int D, int E, bool CU, int MW>
+__global__ void __launch_bounds__(dq_threads<MW>(), 1)
 dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
           const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo, Geom g, AlphaParams ap,
           const float* __restrict__ tau, const float* __restrict__ delta, const int32_t* __restrict__ row_cnt,
@@ -396,7 +405,13 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   using C = Cfg<D>;
   constexpr int NST = (D == 64) ? 5 : 2;   // K/V stages
   constexpr int NDS = (D == 64) ? 2 : 1;
-  constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dS is kDS·dS (exact doubling)   // dS buffers in TMEM: the math warps write dS(k+1) while dQ(k) runs
+  constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dS is kDS·dS (exact doubling)
+  constexpr int kMath = 32 * MW;
+  constexpr int SL = MW / 4;           // key-column slices
+  constexpr int CW = 128 / SL;         // key columns per thread
+  constexpr int NH = CW / 32;
+  constexpr int WPR = CW / 2;          // bf16x2 words of dS per thread
+  constexpr int PROD = MW, MMAW = MW + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
@@ -419,9 +434,9 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       ptx::mbar_init(&kv_empty[s], 1);
     }
     ptx::mbar_init(&s_full, 1);
-    ptx::mbar_init(&s_empty, 8);
+    ptx::mbar_init(&s_empty, MW);
     for (int s = 0; s < NDS; ++s) {
-      ptx::mbar_init(&ds_full[s], 8);
+      ptx::mbar_init(&ds_full[s], MW);
       ptx::mbar_init(&ds_empty[s], 1);
     }
     ptx::mbar_init(&acc_full, 1);
@@ -432,7 +447,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     reinterpret_cast<uint32_t*>(sOnes)[w] = 0x3f803f80u;   // bf16 1.0 pairs
   ptx::fence_proxy_async_smem();                           // visible to the tcgen05.mma operand reads
   if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8002);
-  if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
+  if (warp == MMAW) ptx::tmem_alloc<512>(&tmem_base_sh);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -445,7 +460,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   const int cnt = dense ? g.visible_kblocks(i) : row_cnt[li];
   const BlockList list{dense ? nullptr : row_idx + li * g.Tc, 0};
 
-  if (warp == 8) {
+  if (warp == PROD) {
     ptx::tma_prefetch_desc(&tk);
     ptx::tma_prefetch_desc(&tv);
     ptx::mbar_arrive_expect_tx_elect(&bar_q, 2 * C::TILE);
@@ -464,7 +479,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], jb * kBc, h, b);
 #endif
     }
-  } else if (warp == 9) {
+  } else if (warp == MMAW) {
     ptx::mbar_wait(&bar_q, 0);
     auto issue_sdp = [&](int k) {
       const int st = k % NST;
@@ -505,25 +520,26 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     for (int k = 0; k < cnt; ++k) {
       const int jb = list[k];
       const bool masked = (jb + 1) * kBc - 1 > cta_last;
-      const int key0 = jb * kBc + wg * 64;
+      const int key0 = jb * kBc + wg * CW;
       ptx::mbar_wait(&s_full, k & 1);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 3);
       ptx::tc_fence_after();
-      uint32_t pd[32];
+      uint32_t pd[WPR];
       const float2 cp2 = make_float2(ap.cp, ap.cp), ntr2 = make_float2(-tr, -tr), ndl2 = make_float2(-dl, -dl);
       // all 64 columns of S and dP at once: the buffers are released right after one TMEM latency, so
       // S/dP(k+1) run on the tensor pipe while this warp computes tile k
-      float sa[2][32], da[2][32];
-      ld32f_nowait(lane_base + t_s + wg * 64, sa[0]);
-      ld32f_nowait(lane_base + t_dp + wg * 64, da[0]);
-      ld32f_nowait(lane_base + t_s + wg * 64 + 32, sa[1]);
-      ld32f_nowait(lane_base + t_dp + wg * 64 + 32, da[1]);
+      float sa[NH][32], da[NH][32];
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        ld32f_nowait(lane_base + t_s + wg * CW + hh * 32, sa[hh]);
+        ld32f_nowait(lane_base + t_dp + wg * CW + hh * 32, da[hh]);
+      }
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
       warp_arrive(&s_empty);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 4);
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
+      for (int hh = 0; hh < NH; ++hh) {
         const float(&s)[32] = sa[hh];
         const float(&dp)[32] = da[hh];
         auto body = [&](auto masked_c) {
@@ -566,7 +582,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       if (!seen) {   // (sign bits masked: U = 0 gives dS = ±0)
         uint32_t orv = 0;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) orv |= pd[e];
+        for (int e = 0; e < WPR; ++e) orv |= pd[e];
         seen = __any_sync(0xffffffffu, (orv & 0x7fff7fffu) != 0u);
         if (seen && lane == 0) atomicMin(&s_first, k);
       }
@@ -574,7 +590,8 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       ptx::mbar_wait(&ds_empty[db], ((k / NDS) & 1) ^ 1);   // dQ(k−NDS) has consumed this dS buffer
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 5);
       ptx::tc_fence_after();
-      ptx::tmem_st32(lane_base + t_ds + 64 * db + wg * 32, pd);
+      if constexpr (WPR == 32) ptx::tmem_st32(lane_base + t_ds + 64 * db + wg * WPR, pd);
+      else ptx::tmem_st16(lane_base + t_ds + 64 * db + wg * WPR, pd);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       warp_arrive(&ds_full[db]);
@@ -592,19 +609,18 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     // leak correction (reading r12): dQ_i = c·Σ_j dŜ_ij (K_j − K̄) = c·(acc_i − ρ_i·K̄), exact in real
     // arithmetic for any K̄ because Σ_j dS_ij = 0 (definition of δ); K̄ = mean key of the
     // CTA's first block with a non-zero dS removes the rounding leak's component along the support's keys
-    ptx::named_bar_sync(1, kFbMath);
+    ptx::named_bar_sync(1, kMath);
     const int kf = s_first;
+    constexpr int DS = D / SL;   // dQ columns stored per thread
     const float* kb = (kf == INT_MAX || kbar == nullptr) ? nullptr
-                      : kbar + ((long long)bh * g.Tc + list[kf]) * D + wg * (D / 2);
-    store_row_bf16_corr<D / 2>(lane_base + t_dq + wg * (D / 2),
-                               dq + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2), ap.scale / kDS, cnt == 0,
-                               valid,
-                               rho, kb);
+                      : kbar + ((long long)bh * g.Tc + list[kf]) * D + wg * DS;
+    store_row_bf16_corr<DS>(lane_base + t_dq + wg * DS, dq + g.head_off(bh) + (long long)row * g.sn + wg * DS,
+                            ap.scale / kDS, cnt == 0, valid, rho, kb);
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8003);
-  if (warp == 9) ptx::tmem_dealloc<512>(tmem);
+  if (warp == MMAW) ptx::tmem_dealloc<512>(tmem);
 }
 
 // Store NC fp32 TMEM columns of one row as bf16 × scale (16-column TMEM loads; warp-collective loads, only
