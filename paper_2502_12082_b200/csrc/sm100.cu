@@ -13,7 +13,7 @@ namespace {
 
 template <int D>
 constexpr size_t out_smem(int Tc) {
-  return 1024 + Cfg<D>::TILE + ((D == 64) ? 6 : 2) * 2 * Cfg<D>::TILE + kFbMath * 4 + (size_t)Tc;
+  return 1024 + Cfg<D>::TILE + ((D == 64) ? 6 : 2) * 2 * Cfg<D>::TILE + 2 * kFbMath * 4 + (size_t)Tc;
 }
 template <int D>
 constexpr size_t dkdv_smem() {
@@ -24,6 +24,10 @@ constexpr size_t dq_smem() {
   return 1024 + 2 * Cfg<D>::TILE + ((D == 64) ? 5 : 2) * 2 * Cfg<D>::TILE + kOnesBytes;
 }
 
+#ifndef ENTMAX_OUT_MW
+#define ENTMAX_OUT_MW 8     // math warps of the (1-SM) output kernel (16 measured 1.03 -> 1.05 ms at config 2)
+#endif
+constexpr int kOutMW = ENTMAX_OUT_MW;
 #ifndef ENTMAX_DQ_MW
 #define ENTMAX_DQ_MW 8      // math warps of the dQ kernel (16 measured slower: 1.075 -> 1.133 ms at config 2)
 #endif
@@ -95,15 +99,15 @@ int fwd_t(const void* q, const void* k, const void* v, const Geom& g, const Alph
 #endif
   const size_t sm = out_smem<D>(g.Tc);
   if (o2 != nullptr) {
-    if (int rc = set_smem(out_kernel<D, E, true, CU>, sm)) return rc;
+    if (int rc = set_smem(out_kernel<D, E, true, CU, kOutMW>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    if (cudaError_t e = launch_pdl(out_kernel<D, E, true, CU>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
+    if (cudaError_t e = launch_pdl(out_kernel<D, E, true, CU, kOutMW>, grid, dim3(out_threads<kOutMW>()), sm, st, tq, tk, tv, g, ap, tau,
                                    cand_cnt, cand_idx, (__nv_bfloat16*)o, (float*)o2, mask, row_cnt, row_idx))
       return fail(ENTMAX_ERR_CUDA, "out_sm100 launch: %s", cudaGetErrorString(e));
   } else {
-    if (int rc = set_smem(out_kernel<D, E, false, CU>, sm)) return rc;
+    if (int rc = set_smem(out_kernel<D, E, false, CU, kOutMW>, sm)) return rc;
     ProfScope ps("out_sm100", st);
-    if (cudaError_t e = launch_pdl(out_kernel<D, E, false, CU>, grid, dim3(kFbThreads), sm, st, tq, tk, tv, g, ap, tau,
+    if (cudaError_t e = launch_pdl(out_kernel<D, E, false, CU, kOutMW>, grid, dim3(out_threads<kOutMW>()), sm, st, tq, tk, tv, g, ap, tau,
                                    cand_cnt, cand_idx, (__nv_bfloat16*)o, (float*)nullptr, mask, row_cnt, row_idx))
       return fail(ENTMAX_ERR_CUDA, "out_sm100 launch: %s", cudaGetErrorString(e));
   }

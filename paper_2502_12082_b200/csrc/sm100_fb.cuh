@@ -117,6 +117,34 @@ __device__ __forceinline__ void store_row_bf16(uint32_t taddr, __nv_bfloat16* ds
   }
 }
 
+// Store NC fp32 TMEM columns of one row as bf16 × scale (16-column TMEM loads; warp-collective loads, only
+// lanes with do_store write).
+template <int NC>
+__device__ __forceinline__ void store_cols_bf16(uint32_t taddr, __nv_bfloat16* dst, float scale, bool zero,
+                                                bool do_store) {
+#pragma unroll 1
+  for (int c = 0; c < NC / 16; ++c) {
+    uint32_t r[16];
+    if (!zero) {
+      ptx::tmem_ld16(taddr + c * 16, r);
+      ptx::tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) r[e] = 0u;
+    }
+    if (!do_store) continue;
+    uint4* p = reinterpret_cast<uint4*>(dst + c * 16);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        w[e] = ptx::pack_bf16(__uint_as_float(r[8 * q + 2 * e]) * scale, __uint_as_float(r[8 * q + 2 * e + 1]) * scale);
+      p[q] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
 // dQ epilogue with the leak correction (reading r12): row ← c·(acc − ρ·K̄) for NC fp32 columns (16-column
 // TMEM loads), K̄ = kb[0..NC) (fp32, global), ρ this row's Σ_j dŜ_ij.
 template <int NC>
@@ -166,8 +194,13 @@ __device__ __forceinline__ void store_row_bf16_corr(uint32_t taddr, __nv_bfloat1
 // keeps the tensor pipe on later tiles while the math warps work on the current one; S(k+NSB) is issued
 // after PV(k) in program order, so the in-order tensor pipe never overwrites P(k) before it is consumed.
 // =====================================================================================
-template <int D, int E, bool TRAIN, bool CU>
-__global__ void __launch_bounds__(kFbThreads, 1)
+template <int MW>
+constexpr int out_threads() { return 32 * MW + 64; }
+
+// MW math warps (8 or 16): warp w owns TMEM lanes 32·(w & 3) and the key-column slice w >> 2 of width
+// CW = 128·4/MW, whose first CW/4 columns it overwrites with P and the next CW/4 with U.
+template <int D, int E, bool TRAIN, bool CU, int MW>
+__global__ void __launch_bounds__(out_threads<MW>(), 1)
 out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
            const __grid_constant__ CUtensorMap tv, Geom g, AlphaParams ap, const float* __restrict__ tau,
            const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx, __nv_bfloat16* __restrict__ o,
@@ -179,12 +212,17 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   // (d = 64: 3 × 128 + O 64 + O⁽²⁾ 64; inference d = 128: 3 × 128 + O 128), so S(k+3) runs while the math
   // warps still work on tiles k+1 and k+2
   constexpr int NSB = (D == 64 || !TRAIN) ? 3 : 2;
+  constexpr int kMath = 32 * MW;
+  constexpr int SL = MW / 4;           // key-column slices
+  constexpr int CW = 128 / SL;         // key columns per thread
+  constexpr int WPR = CW / 2;          // bf16x2 words of P (and of U) per thread
+  constexpr int PROD = MW, MMAW = MW + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sKV = sQ + C::TILE;                  // NST × [K tile | V tile]
-  float* xch = reinterpret_cast<float*>(sKV + NST * 2 * C::TILE);   // [256]
-  uint8_t* aflag = reinterpret_cast<uint8_t*>(xch + kFbMath);       // [Tc]
+  float* xch = reinterpret_cast<float*>(sKV + NST * 2 * C::TILE);   // [kMath]
+  uint8_t* aflag = reinterpret_cast<uint8_t*>(xch + kMath);         // [Tc]
   __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full[NSB], p_full[NSB], o_full;
   __shared__ uint32_t tmem_base_sh;
 
@@ -201,14 +239,14 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
     for (int s = 0; s < NSB; ++s) {
       ptx::mbar_init(&s_full[s], 1);
-      ptx::mbar_init(&p_full[s], 8);
+      ptx::mbar_init(&p_full[s], MW);
     }
     ptx::mbar_init(&o_full, 1);
     ptx::fence_mbar_init();
   }
   for (int j = threadIdx.x; j < g.Tc; j += blockDim.x) aflag[j] = 0;
   if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8002);
-  if (warp == 9) ptx::tmem_alloc<512>(&tmem_base_sh);
+  if (warp == MMAW) ptx::tmem_alloc<512>(&tmem_base_sh);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -220,7 +258,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   const int ncand = dense ? g.visible_kblocks(i) : cand_cnt[li];
   const BlockList list{dense ? nullptr : cand_idx + li * g.Tc, 0};
 
-  if (warp == 8) {
+  if (warp == PROD) {
     ptx::tma_prefetch_desc(&tq);
     ptx::tma_prefetch_desc(&tk);
     ptx::tma_prefetch_desc(&tv);
@@ -239,7 +277,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       tma_tile<D>(sKV + st * 2 * C::TILE + C::TILE, &tv, &kv_full[st], j * kBc, h, b);
 #endif
     }
-  } else if (warp == 9) {
+  } else if (warp == MMAW) {
     ptx::mbar_wait(&bar_q, 0);
     auto issue_s = [&](int k) {
       const int st = k % NST;
@@ -257,8 +295,11 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       ptx::tc_fence_after();
       const uint32_t buf = tmem + sb * 128;
       const uint8_t* sV = sKV + st * 2 * C::TILE + C::TILE;
-      mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
-      if (TRAIN) mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + 32 + 8 * ks + (ks >= 4 ? 32 : 0); }, sV, k > 0);
+      // k-step ks (16 keys = 8 words) lives in slice ks / KPS: P at its start, U CW/4 columns later
+      constexpr int KPS = CW / 16;
+      mma_tmem_x_tile<D>(t_o, [&](int ks) { return buf + CW * (ks / KPS) + 8 * (ks % KPS); }, sV, k > 0);
+      if (TRAIN)
+        mma_tmem_x_tile<D>(t_o2, [&](int ks) { return buf + CW * (ks / KPS) + WPR + 8 * (ks % KPS); }, sV, k > 0);
       ptx::mma_commit_elect(&kv_empty[st]);
       if (k + NSB < ncand) issue_s(k + NSB);
     }
@@ -275,22 +316,22 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     for (int k = 0; k < ncand; ++k) {
       const int j = list[k], sb = k % NSB;
       const bool masked = (j + 1) * kBc - 1 > cta_last;
-      const uint32_t col = lane_base + sb * 128 + wg * 64;
+      const uint32_t col = lane_base + sb * 128 + wg * CW;
       ptx::mbar_wait(&s_full[sb], (k / NSB) & 1);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 3);
       ptx::tc_fence_after();
       float s0[32], s1[32];
       ld32f_nowait(col, s0);
-      ld32f_nowait(col + 32, s1);
+      if constexpr (CW == 64) ld32f_nowait(col + 32, s1);
       ptx::tmem_wait_ld();
-      uint32_t pp[32], pu[32];
+      uint32_t pp[WPR], pu[WPR];
       float2 su = make_float2(0.f, 0.f);     // Σ U of this step (> 0 ⟺ some x > 0 for E ∈ {1, 2})
       float xmax = -INFINITY;
       const float2 cp2 = make_float2(ap.cp, ap.cp), ntr2 = make_float2(-tr, -tr);
-      const int key0 = j * kBc + wg * 64;
+      const int key0 = j * kBc + wg * CW;
       auto body = [&](auto masked_c) {
 #pragma unroll
-        for (int e = 0; e < 64; e += 2) {
+        for (int e = 0; e < CW; e += 2) {
           float2 x = ffma2(make_float2(e < 32 ? s0[e] : s1[e - 32], e < 32 ? s0[e + 1] : s1[e - 31]), cp2, ntr2);
           if constexpr (decltype(masked_c)::value) {
             if (key0 + e > my_last) x.x = kMaskX;
@@ -333,8 +374,13 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       usum += su.x + su.y;
       if (E == 1 || E == 2) xmax = su.x + su.y;   // exact: every U > 0 iff x > 0 (no underflow for e <= 2)
       if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 4);
-      ptx::tmem_st32(col, pp);
-      if (TRAIN) ptx::tmem_st32(col + 32, pu);
+      if constexpr (WPR == 32) {
+        ptx::tmem_st32(col, pp);
+        if (TRAIN) ptx::tmem_st32(col + 32, pu);
+      } else {
+        ptx::tmem_st16(col, pp);
+        if (TRAIN) ptx::tmem_st16(col + 16, pu);
+      }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
       warp_arrive(&p_full[sb]);
@@ -343,36 +389,42 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     }
     // epilogue: O and O⁽²⁾ = (Σ U V)/ΣU; each column half written by its warpgroup
     xch[tid] = usum;
-    ptx::named_bar_sync(1, kFbMath);
-    const float inv = 1.0f / (xch[r] + xch[128 + r]);
+    ptx::named_bar_sync(1, kMath);
+    float usr = 0.f;
+#pragma unroll
+    for (int q = 0; q < SL; ++q) usr += xch[q * 128 + r];
+    const float inv = 1.0f / usr;
     if (ncand > 0) {
       ptx::mbar_wait(&o_full, 0);
       ptx::tc_fence_after();
     }
-    store_row_bf16<D / 2>(lane_base + 128 * NSB + wg * (D / 2), o + g.head_off(bh) + (long long)row * g.sn + wg * (D / 2),
-                          1.0f, ncand == 0, valid);
+    constexpr int DS = D / SL;   // O / O⁽²⁾ columns stored per thread
+    store_cols_bf16<DS>(lane_base + 128 * NSB + wg * DS, o + g.head_off(bh) + (long long)row * g.sn + wg * DS, 1.0f,
+                        ncand == 0, valid);
     if (TRAIN) {
 #pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        float v[32];
+      for (int c = 0; c < DS / 16; ++c) {
+        uint32_t rv[16];
         if (ncand > 0) {
-          ld_chunk(lane_base + 128 * NSB + D + wg * (D / 2) + c * 32, v);
+          ptx::tmem_ld16(lane_base + 128 * NSB + D + wg * DS + c * 16, rv);
+          ptx::tmem_wait_ld();
         } else {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0.f;
+          for (int e = 0; e < 16; ++e) rv[e] = 0u;
         }
         if (valid) {
-          float4* dst = reinterpret_cast<float4*>(o2 + ((long long)bh * g.N + row) * D + wg * (D / 2) + c * 32);
+          float4* dst = reinterpret_cast<float4*>(o2 + ((long long)bh * g.N + row) * D + wg * DS + c * 16);
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            dst[q] = make_float4(v[4 * q] * inv, v[4 * q + 1] * inv, v[4 * q + 2] * inv, v[4 * q + 3] * inv);
+          for (int q = 0; q < 4; ++q)
+            dst[q] = make_float4(__uint_as_float(rv[4 * q]) * inv, __uint_as_float(rv[4 * q + 1]) * inv,
+                                 __uint_as_float(rv[4 * q + 2]) * inv, __uint_as_float(rv[4 * q + 3]) * inv);
         }
       }
     }
     if (!dense) {
-      ptx::named_bar_sync(1, kFbMath);
+      ptx::named_bar_sync(1, kMath);
       uint8_t* mrow = mask + li * g.Tc;
-      for (int j = tid; j < g.Tc; j += kFbMath) mrow[j] = aflag[j];
+      for (int j = tid; j < g.Tc; j += kMath) mrow[j] = aflag[j];
       if (warp == 0) {
         const int cnt = compact_flags(aflag, g.Tc, row_idx + li * g.Tc);
         if (lane == 0) row_cnt[li] = cnt;
@@ -382,7 +434,7 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8003);
-  if (warp == 9) ptx::tmem_dealloc<512>(tmem);
+  if (warp == MMAW) ptx::tmem_dealloc<512>(tmem);
 }
 
 // =====================================================================================
@@ -621,34 +673,6 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   __syncthreads();
   if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8003);
   if (warp == MMAW) ptx::tmem_dealloc<512>(tmem);
-}
-
-// Store NC fp32 TMEM columns of one row as bf16 × scale (16-column TMEM loads; warp-collective loads, only
-// lanes with do_store write).
-template <int NC>
-__device__ __forceinline__ void store_cols_bf16(uint32_t taddr, __nv_bfloat16* dst, float scale, bool zero,
-                                                bool do_store) {
-#pragma unroll 1
-  for (int c = 0; c < NC / 16; ++c) {
-    uint32_t r[16];
-    if (!zero) {
-      ptx::tmem_ld16(taddr + c * 16, r);
-      ptx::tmem_wait_ld();
-    } else {
-#pragma unroll
-      for (int e = 0; e < 16; ++e) r[e] = 0u;
-    }
-    if (!do_store) continue;
-    uint4* p = reinterpret_cast<uint4*>(dst + c * 16);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      uint32_t w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        w[e] = ptx::pack_bf16(__uint_as_float(r[8 * q + 2 * e]) * scale, __uint_as_float(r[8 * q + 2 * e + 1]) * scale);
-      p[q] = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-  }
 }
 
 // =====================================================================================
