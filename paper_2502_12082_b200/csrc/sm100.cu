@@ -31,9 +31,6 @@ constexpr int kOutMW = ENTMAX_OUT_MW;
 #ifndef ENTMAX_DQ_MW
 #define ENTMAX_DQ_MW 8      // math warps of the dQ kernel (16 measured slower: 1.075 -> 1.133 ms at config 2)
 #endif
-#ifndef ENTMAX_DKDV2
-#define ENTMAX_DKDV2 0      // dK/dV on CTA pairs with 2-SM MMAs (parity green; measured slower: config 5 7.6 -> 9.0 ms)
-#endif
 #ifndef ENTMAX_DKDV_MW
 #define ENTMAX_DKDV_MW 16   // math warps of the dK/dV kernel (8: 1.64 ms, 16: 1.43 ms at config 2)
 #endif
@@ -124,28 +121,6 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
           cudaStream_t st) {
   CUtensorMap tq, tk, tv, tdo;
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
-#if ENTMAX_DKDV2
-  if (g.Tr <= 1024) {
-    // dK/dV on CTA pairs (2-SM MMAs, sm100_fb2.cuh): Q, dO as 64-query K-major halves and d/2-column
-    // MN-major halves (SW64 boxes at d = 64)
-    CUtensorMap tq64, tdo64, tqh, tdoh;
-    bool ok = make_tmap_bhnd(&tq64, q, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn, 64) &&
-              make_tmap_bhnd(&tdo64, dO, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn, 64);
-    ok = ok && (D == 64 ? make_tmap_bhnd_sw64(&tqh, q, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn) &&
-                              make_tmap_bhnd_sw64(&tdoh, dO, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn)
-                        : make_tmap_bhnd(&tqh, q, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn) &&
-                              make_tmap_bhnd(&tdoh, dO, g.B, g.H, g.N, g.d, g.sb, g.sh, g.sn));
-    if (!ok) return fail(ENTMAX_ERR_INVALID_ARG, "cuTensorMapEncodeTiled failed (Q/dO halves)");
-    constexpr int MW = ENTMAX_DKDV_MW;
-    const size_t sm = Dkdv2Cfg<D>::smem();
-    if (int rc = set_smem(dkdv2_kernel<D, E, CU, MW>, sm)) return rc;
-    ProfScope ps("dkdv_sm100", st);
-    if (cudaError_t e = launch_pdl(dkdv2_kernel<D, E, CU, MW>, dim3((g.Tc + 1) & ~1, g.B * g.H), dim3(dkdv_threads<MW>()),
-                                   sm, st, tq64, tk, tv, tdo64, tqh, tdoh, g, ap, td, col_cnt, col_idx, kbar,
-                                   (__nv_bfloat16*)dk, (__nv_bfloat16*)dv))
-      return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
-  } else
-#endif
   {
     const size_t sm = dkdv_smem<D>();
     constexpr int MW = ENTMAX_DKDV_MW;

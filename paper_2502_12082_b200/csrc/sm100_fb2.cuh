@@ -288,323 +288,5 @@ out2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   if (warp == 9) ptx::tmem_dealloc_2sm<512>(tmem);
 }
 
-// =====================================================================================
-// dK_j, dV_j over 𝒦_j (Alg. 4) on CTA pairs with 2-SM MMAs: the two key blocks j, j+1 of a cluster pair
-// share every Q_i / dO_i tile and every MMA.  The even CTA issues M = 256 MMAs whose A rows are each CTA's
-// own keys (K, V in shared memory for Sᵀ, dPᵀ; Pᵀ, dSᵀ in TMEM for dV, dK) and whose B columns are split:
-// each CTA holds the 64-query half of Q_i and dO_i (K-major, for Sᵀ / dPᵀ) and the d/2-column half of
-// Q_i and dO_i (MN-major: SW64 at d = 64, SW128 at d = 128, for dK / dV).  The pair visits 𝒦_j ∪ 𝒦_j+1
-// (a query block outside a CTA's own list gives its keys P = dS = 0 exactly; causal: a query block below
-// the CTA's key block is masked whole).  τ_i, δ_i arrive in each CTA by its own bulk copy.
-// =====================================================================================
-template <int D>
-struct Dkdv2Cfg {
-  static constexpr uint32_t QHALF = Cfg<D>::KCH * (kChunkBytes / 2);   // 64 queries × D
-  static constexpr uint32_t DHALF = 128u * (D / 2) * 2u;                 // 128 queries × D/2
-  static constexpr uint32_t TD = 2 * kBr * 4;                             // τ_i[128] | δ_i[128]
-  // stage: Q q-half | dO q-half | Q d-half | dO d-half | τ/δ
-  static constexpr uint32_t STAGE = 2 * QHALF + 2 * DHALF + TD;
-  static constexpr int NST = (D == 64) ? 5 : 2;
-  static constexpr size_t smem() { return 1024 + 2 * Cfg<D>::TILE + (size_t)NST * STAGE; }
-};
-
-template <int D, int E, bool CU, int MW>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(dkdv_threads<MW>(), 1)
-dkdv2_kernel(const __grid_constant__ CUtensorMap tq64, const __grid_constant__ CUtensorMap tk,
-             const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tdo64,
-             const __grid_constant__ CUtensorMap tqh, const __grid_constant__ CUtensorMap tdoh, Geom g, AlphaParams ap,
-             const float* __restrict__ td, const int32_t* __restrict__ col_cnt, const int32_t* __restrict__ col_idx,
-             float* __restrict__ kbar, __nv_bfloat16* __restrict__ dk, __nv_bfloat16* __restrict__ dv) {
-  using C = Cfg<D>;
-  using DC = Dkdv2Cfg<D>;
-  constexpr bool ALIAS = (D == 128);
-  constexpr int NST = DC::NST;
-  constexpr float kDS = ((E == 2 || E == 4) && !CU) ? 2.f : 1.f;   // the stored dSᵀ is kDS·dSᵀ (exact doubling)
-  constexpr int kMath = 32 * MW;
-  constexpr int SL = MW / 4;           // query-column slices
-  constexpr int CW = 128 / SL;         // query columns per thread
-  constexpr int NH = CW / 32;
-  constexpr int WPR = CW / 2;
-  constexpr int KPS = CW / 16;
-  constexpr int PROD = MW, MMAW = MW + 1;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint8_t* sK = smem;
-  uint8_t* sV = sK + C::TILE;
-  uint8_t* sStage = sV + C::TILE;
-  __shared__ __align__(8) uint64_t bar_kv, qd_full[NST], td_full[NST], qd_empty[NST], s_full, s_empty, p_full,
-      p_empty, acc_full;
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ int s_ucnt;
-  __shared__ int32_t ulist[1024];   // union of the pair's 𝒦 lists (T_r <= 1024 on this path)
-  __shared__ uint8_t uflag[1024];
-
-  const int j = blockIdx.x, bh = blockIdx.y;
-  const int b = bh / g.H, h = bh - b * g.H;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank();
-  const int pair0 = j & ~1;
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(&bar_kv, 1);
-    for (int s = 0; s < NST; ++s) {
-      ptx::mbar_init(&qd_full[s], 1);
-      ptx::mbar_init(&td_full[s], 1);
-      ptx::mbar_init(&qd_empty[s], 1);
-    }
-    ptx::mbar_init(&s_full, 1);
-    ptx::mbar_init(&s_empty, 2 * MW);
-    ptx::mbar_init(&p_full, 2 * MW);
-    ptx::mbar_init(&p_empty, 1);
-    ptx::mbar_init(&acc_full, 1);
-    ptx::fence_mbar_init();
-  }
-  for (int e = threadIdx.x; e < g.Tr; e += blockDim.x) uflag[e] = 0;
-  if (warp == MMAW) ptx::tmem_alloc_2sm<512>(&tmem_base_sh);
-  ptx::tc_fence_before();
-  ptx::cluster_sync();
-  ptx::tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-  const uint32_t t_s = tmem, t_dp = tmem + 128;
-  ptx::griddep_launch_dependents();
-  ptx::griddep_wait();   // δ and the 𝒦 tables are complete
-  const bool dense = col_idx == nullptr;
-  const int i0 = g.causal ? (pair0 * kBc) / kBr : 0;
-  int ucnt;
-  if (dense) {
-    ucnt = g.Tr - i0;
-  } else {
-    for (int q = 0; q < 2; ++q) {
-      const int jq = pair0 + q;
-      if (jq >= g.Tc) continue;
-      const long long lq = (long long)bh * g.Tc + jq;
-      const int n = col_cnt[lq];
-      for (int e = threadIdx.x; e < n; e += blockDim.x) uflag[col_idx[lq * g.Tr + e]] = 1;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const int n = compact_flags(uflag, g.Tr, ulist);
-      if (lane == 0) s_ucnt = n;
-    }
-    __syncthreads();
-    ucnt = s_ucnt;
-  }
-  auto ublock = [&](int k) { return dense ? i0 + k : ulist[k]; };
-  const uint32_t t_dv = tmem + (ALIAS ? 256 : 384), t_dk = t_dv + D;
-  auto pt_col = [&](int ks) { return ALIAS ? t_s + CW * (ks / KPS) + 8 * (ks % KPS) : tmem + 256 + 8 * ks; };
-  auto dst_col = [&](int ks) { return ALIAS ? t_dp + CW * (ks / KPS) + 8 * (ks % KPS) : tmem + 320 + 8 * ks; };
-
-  if (warp == PROD) {
-    // ---------------------------------------------------------------- TMA producer (both CTAs)
-    if (rank == 0) ptx::mbar_arrive_expect_tx_elect(&bar_kv, 4 * C::TILE);
-    const uint32_t barkv_c = ptx::mapa(ptx::smem_u32(&bar_kv), 0);
-#pragma unroll
-    for (int c = 0; c < C::KCH; ++c) {
-      ptx::tma_load_4d_2sm_elect(sK + c * kChunkBytes, &tk, barkv_c, c * 64, j * kBc, h, b);
-      ptx::tma_load_4d_2sm_elect(sV + c * kChunkBytes, &tv, barkv_c, c * 64, j * kBc, h, b);
-    }
-    for (int k = 0; k < ucnt; ++k) {
-      const int ib = ublock(k), st = k % NST;
-      uint8_t* stg = sStage + st * DC::STAGE;
-      ptx::mbar_wait(&qd_empty[st], ((k / NST) & 1) ^ 1);
-      ptx::mbar_arrive_expect_tx_elect(&td_full[st], DC::TD);
-      ptx::bulk_load_elect(stg + 2 * DC::QHALF + 2 * DC::DHALF, td + ((long long)bh * g.Tr + ib) * (2 * kBr), DC::TD,
-                           &td_full[st]);
-      if (rank == 0) ptx::mbar_arrive_expect_tx_elect(&qd_full[st], 2 * (2 * DC::QHALF + 2 * DC::DHALF));
-      const uint32_t full_c = ptx::mapa(ptx::smem_u32(&qd_full[st]), 0);
-#pragma unroll
-      for (int c = 0; c < C::KCH; ++c) {   // this CTA's 64 queries of Q_i, dO_i (K-major)
-        ptx::tma_load_4d_2sm_elect(stg + c * (kChunkBytes / 2), &tq64, full_c, c * 64, ib * kBr + (int)rank * 64, h, b);
-        ptx::tma_load_4d_2sm_elect(stg + DC::QHALF + c * (kChunkBytes / 2), &tdo64, full_c, c * 64,
-                                   ib * kBr + (int)rank * 64, h, b);
-      }
-      // this CTA's d/2 columns of Q_i, dO_i (all 128 queries; MN-major)
-      ptx::tma_load_4d_2sm_elect(stg + 2 * DC::QHALF, &tqh, full_c, (int)rank * (D / 2), ib * kBr, h, b);
-      ptx::tma_load_4d_2sm_elect(stg + 2 * DC::QHALF + DC::DHALF, &tdoh, full_c, (int)rank * (D / 2), ib * kBr, h, b);
-    }
-  } else if (warp == MMAW) {
-    // ---------------------------------------------------------------- MMA issuer (leader CTA only)
-    if (rank == 0) {
-      ptx::mbar_wait(&bar_kv, 0);
-      constexpr uint32_t idesc_s = ptx::idesc_bf16(256, 128, 0, 0);
-      constexpr uint32_t idesc_g = ptx::idesc_bf16(256, D, 0, 1);
-      auto issue_sdp = [&](int k) {
-        const int st = k % NST;
-        const uint32_t stg = ptx::smem_u32(sStage + st * DC::STAGE);
-        ptx::mbar_wait(&qd_full[st], (k / NST) & 1);
-        if (!ALIAS) ptx::mbar_wait_cluster(&s_empty, (k & 1) ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t sk = ptx::smem_u32(sK), sv = ptx::smem_u32(sV);
-#pragma unroll
-        for (int ks = 0; ks < C::KSTEPS; ++ks) {
-          const uint32_t ao = (ks >> 2) * kChunkBytes + (ks & 3) * 32, bo = (ks >> 2) * (kChunkBytes / 2) + (ks & 3) * 32;
-          ptx::mma2_bf16_ss_elect(t_s, ptx::sdesc_kmajor(sk + ao), ptx::sdesc_kmajor(stg + bo), idesc_s, ks > 0 ? 1u : 0u);
-        }
-#pragma unroll
-        for (int ks = 0; ks < C::KSTEPS; ++ks) {
-          const uint32_t ao = (ks >> 2) * kChunkBytes + (ks & 3) * 32, bo = (ks >> 2) * (kChunkBytes / 2) + (ks & 3) * 32;
-          ptx::mma2_bf16_ss_elect(t_dp, ptx::sdesc_kmajor(sv + ao), ptx::sdesc_kmajor(stg + DC::QHALF + bo), idesc_s,
-                                  ks > 0 ? 1u : 0u);
-        }
-        ptx::mma2_commit_mc_elect(&s_full, 0x3);
-      };
-      // B = this CTA's d-half of dO_i / Q_i, MN-major over the 128 queries (K-step of 16 queries)
-      auto hdesc = [&](uint32_t sh, int ks) {
-        if constexpr (D == 64) return ptx::sdesc_mnmajor_sw64(sh + ks * 1024);
-        else return ptx::sdesc_mnmajor(sh + ks * 2048, kChunkBytes);
-      };
-      if (ucnt > 0) issue_sdp(0);
-      for (int k = 0; k < ucnt; ++k) {
-        if (!ALIAS && k + 1 < ucnt) issue_sdp(k + 1);
-        const int st = k % NST;
-        const uint32_t stg = ptx::smem_u32(sStage + st * DC::STAGE);
-        ptx::mbar_wait_cluster(&p_full, k & 1);
-        ptx::tc_fence_after();
-        const uint32_t sqh = stg + 2 * DC::QHALF, sdoh = sqh + DC::DHALF;
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)   // dV += Pᵀ dO_i
-          ptx::mma2_bf16_ts_elect(t_dv, pt_col(ks), hdesc(sdoh, ks), idesc_g, (k > 0 || ks > 0) ? 1u : 0u);
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks)   // dK += dSᵀ Q_i
-          ptx::mma2_bf16_ts_elect(t_dk, dst_col(ks), hdesc(sqh, ks), idesc_g, (k > 0 || ks > 0) ? 1u : 0u);
-        ptx::mma2_commit_mc_elect(&qd_empty[st], 0x3);
-        if (!ALIAS) ptx::mma2_commit_mc_elect(&p_empty, 0x3);
-        if (ALIAS && k + 1 < ucnt) issue_sdp(k + 1);
-      }
-      ptx::mma2_commit_mc_elect(&acc_full, 0x3);
-    }
-  } else {
-    // ---------------------------------------------------------------- math warps (both CTAs)
-    const int tid = threadIdx.x, wg = warp >> 2, r = tid & 127;
-    const int key = j * kBc + r;
-    const bool valid = key < g.N;
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t sempty_c = ptx::mapa(ptx::smem_u32(&s_empty), 0), pfull_c = ptx::mapa(ptx::smem_u32(&p_full), 0);
-    for (int k = 0; k < ucnt; ++k) {
-      const int ib = ublock(k), st = k % NST;
-      const uint8_t* stg = sStage + st * DC::STAGE;
-      const uint32_t tq4 = ptx::smem_u32(stg + 2 * DC::QHALF + 2 * DC::DHALF) + wg * (CW * 4);   // τ_i
-      const uint32_t dl4 = tq4 + 512;                                                          // δ_i
-      const bool diag = g.causal && ib == j;          // queries below the key inside the diagonal block
-      const bool below = g.causal && ib < j;          // the whole query block precedes this key block
-      ptx::mbar_wait(&td_full[st], (k / NST) & 1);   // τ_i, δ_i in this CTA
-      ptx::mbar_wait(&s_full, k & 1);
-      ptx::tc_fence_after();
-      uint32_t pp[WPR], pd[WPR];
-      float sa[NH][32], da[NH][32];
-#pragma unroll
-      for (int hh = 0; hh < NH; ++hh) {
-        ld32f_nowait(lane_base + t_s + wg * CW + hh * 32, sa[hh]);
-        ld32f_nowait(lane_base + t_dp + wg * CW + hh * 32, da[hh]);
-      }
-      ptx::tmem_wait_ld();
-      if (!ALIAS) {
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(sempty_c);
-      }
-#pragma unroll
-      for (int hh = 0; hh < NH; ++hh) {
-        const float(&s)[32] = sa[hh];
-        const float(&dp)[32] = da[hh];
-        auto body = [&](auto masked_c) {
-#pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) {
-            const float4 t4 = ld_shared_f4(tq4 + (hh * 8 + q4) * 16), d4 = ld_shared_f4(dl4 + (hh * 8 + q4) * 16);
-#pragma unroll
-            for (int e = 0; e < 4; e += 2) {
-              const float2 tq2 = e == 0 ? make_float2(-t4.x, -t4.y) : make_float2(-t4.z, -t4.w);
-              const float2 dq2 = e == 0 ? make_float2(-d4.x, -d4.y) : make_float2(-d4.z, -d4.w);
-              float2 x = ffma2(make_float2(s[q4 * 4 + e], s[q4 * 4 + e + 1]), make_float2(ap.cp, ap.cp), tq2);
-              if constexpr (decltype(masked_c)::value) {
-                const int ql = wg * CW + hh * 32 + q4 * 4 + e;
-                if (!valid || below || (diag && ql < r)) x.x = kMaskX;
-                if (!valid || below || (diag && ql + 1 < r)) x.y = kMaskX;
-              }
-              const float2 g2 = fadd2(make_float2(dp[q4 * 4 + e], dp[q4 * 4 + e + 1]), dq2);
-              const int w = hh * 16 + q4 * 2 + (e >> 1);
-              if constexpr (E == 2 || E == 4) {
-                uint32_t pb, ub;
-                pu_packed<E>(x, pb, ub);
-                pp[w] = pb;
-                if constexpr (CU) {
-                  pd[w] = mul_bf16x2(ub, ptx::pack_bf16(g2.x, g2.y));
-                } else {
-                  const float2 bb = E == 2 ? x : fmul2(fmul2(x, fabs2(x)), fabs2(x));
-                  const float2 ds2 = fmul2(fadd2(bb, fabs2(bb)), g2);
-                  pd[w] = ptx::pack_bf16(ds2.x, ds2.y);
-                }
-              } else {
-                float2 p, u;
-                p_and_u2<E>(x, ap, p, u);
-                pp[w] = ptx::pack_bf16(p.x, p.y);
-                if constexpr (CU)
-                  pd[w] = mul_bf16x2(ptx::pack_bf16(u.x, u.y), ptx::pack_bf16(g2.x, g2.y));
-                else {
-                  const float2 ds = fmul2(u, g2);
-                  pd[w] = ptx::pack_bf16(ds.x, ds.y);
-                }
-              }
-            }
-          }
-        };
-        if (!valid || diag || below) body(std::true_type{}); else body(std::false_type{});
-      }
-      if (!ALIAS) {
-        ptx::mbar_wait(&p_empty, (k & 1) ^ 1);   // dV/dK(k−1) have consumed the previous Pᵀ, dSᵀ
-        ptx::tc_fence_after();
-      }
-      if constexpr (WPR == 32) {
-        ptx::tmem_st32(lane_base + pt_col(wg * KPS), pp);
-        ptx::tmem_st32(lane_base + dst_col(wg * KPS), pd);
-      } else {
-        ptx::tmem_st16(lane_base + pt_col(wg * KPS), pp);
-        ptx::tmem_st16(lane_base + dst_col(wg * KPS), pd);
-      }
-      ptx::tmem_wait_st();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(pfull_c);
-    }
-    // (the leader commits acc_full after its K/V barrier even when the list is empty, so this wait also
-    // orders the K̄ reads below after this CTA's K tile landed)
-    ptx::mbar_wait(&acc_full, 0);
-    ptx::tc_fence_after();
-    constexpr int DS = D / SL;
-    const long long off = g.head_off(bh) + (long long)(valid ? key : 0) * g.sn + wg * DS;
-    store_cols_bf16<DS>(lane_base + t_dv + wg * DS, dv + off, 1.0f, ucnt == 0, valid);
-    store_cols_bf16<DS>(lane_base + t_dk + wg * DS, dk + off, ap.scale / kDS, ucnt == 0, valid);
-    if (kbar != nullptr && j < g.Tc) {
-      // K̄_j (reading r12) from this CTA's K tile, as in dkdv_kernel
-      constexpr int UNITS = D / 8, RP = kMath / UNITS;
-      const int u = tid % UNITS, rp = tid / UNITS;
-      const uint32_t kb0 = ptx::smem_u32(sK) + (uint32_t)(u >> 3) * kChunkBytes;
-      float a[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = 0.f;
-#pragma unroll 4
-      for (int rr = rp; rr < 128; rr += RP) {
-        const uint4 w = ld_shared_u4(kb0 + ptx::sw128_off(rr, u & 7));
-        const float2 f0 = bf16x2_to_float2(w.x), f1 = bf16x2_to_float2(w.y), f2 = bf16x2_to_float2(w.z),
-                     f3 = bf16x2_to_float2(w.w);
-        a[0] += f0.x; a[1] += f0.y; a[2] += f1.x; a[3] += f1.y;
-        a[4] += f2.x; a[5] += f2.y; a[6] += f3.x; a[7] += f3.y;
-      }
-      float* red = reinterpret_cast<float*>(sStage);   // [RP][D] (the stages are idle now)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) red[rp * D + u * 8 + e] = a[e];
-      ptx::named_bar_sync(1, kMath);
-      if (tid < D) {
-        float sum = 0.f;
-        for (int p = 0; p < RP; ++p) sum += red[p * D + tid];
-        kbar[((long long)bh * g.Tc + j) * D + tid] = sum / (float)min(kBc, g.N - j * kBc);
-      }
-    }
-  }
-  ptx::tc_fence_before();
-  ptx::cluster_sync();
-  if (warp == MMAW) ptx::tmem_dealloc_2sm<512>(tmem);
-}
-
 }  // namespace sm100
 }  // namespace entmax
