@@ -24,6 +24,12 @@
 namespace entmax {
 namespace rowwise {
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 template <typename T>
 struct Chunk;   // one 16-byte vector
 template <>
@@ -165,17 +171,19 @@ __global__ void __launch_bounds__(NT) fwd_reg_kernel(const T* s, int n, long lon
   const long long row = blockIdx.x;
   const T* srow = s + row * ld;
   float z[VPT];
-  // Alg. 1 line 3: z = (α−1)·s; line 4: m = max z (padding entries are −∞: not visible)
+  // Alg. 1 line 3: z = (α−1)·s; line 4: m = max z (padding entries past n: a huge finite negative value,
+  // so they contribute exact zeros — also to the packed sums below, where x + |x| must not meet ∞ − ∞)
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     float v[W];
-    load_chunk<T>(srow, (c * NT + threadIdx.x) * W, n, -INFINITY, v);
+    load_chunk<T>(srow, (c * NT + threadIdx.x) * W, n, -1e30f, v);
 #pragma unroll
     for (int e = 0; e < W; ++e) z[c * W + e] = v[e] * ap.cp;
   }
   float m = z[0];
 #pragma unroll
-  for (int i = 1; i < VPT; ++i) m = fmaxf(m, z[i]);
+  for (int i = 1; i + 1 < VPT; i += 2) m = fmax3(m, z[i], z[i + 1]);
+  if constexpr (VPT % 2 == 0) m = fmaxf(m, z[VPT - 1]);
   m = block_max<NT>(m, red, ph);
   RowState rs = bracket_init(m, (float)n, ap.alpha);   // lines 5-6
   // Candidates (readings c3/c7): every iterate is >= τ_lo = m − 1, so z <= τ_lo gives x = z − τ <= 0
@@ -190,8 +198,45 @@ __global__ void __launch_bounds__(NT) fwd_reg_kernel(const T* s, int n, long lon
   if (!compact) {
     for (int t = 0; t < n_iter; ++t) {
       float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+      if constexpr (E == 1 || E == 2 || E == 4) {
+        // packed f32x2 sums over pairs of values (sm_100a FADD2 / FFMA2 / FMUL2), in doubled units
+        // r = x + |x| = 2·x₊ (exact), rescaled by exact powers of two at the end
+        float2 A0 = make_float2(0.f, 0.f), A1 = A0, A2 = A0;
+        const float2 nt = make_float2(-rs.tau, -rs.tau);
 #pragma unroll
-      for (int i = 0; i < VPT; ++i) accum_f<E>(z[i] - rs.tau, ap, a0, a1, a2);
+        for (int i = 0; i < VPT; i += 2) {
+          const float2 x = fadd2(make_float2(z[i], z[i + 1]), nt);
+          const float2 r = fadd2(x, fabs2(x));
+          if constexpr (E == 1) {          // f = Σx₊ − 1, f' ∝ Σ[x > 0]
+            A0 = fadd2(A0, r);
+            A1 = fadd2(A1, make_float2(fminf(r.x * 0x1p100f, 1.f), fminf(r.y * 0x1p100f, 1.f)));
+          } else if constexpr (E == 2) {   // Σx₊², Σx₊, Σ[x > 0]
+            A0 = ffma2(r, r, A0);
+            A1 = fadd2(A1, r);
+            A2 = fadd2(A2, make_float2(fminf(r.x * 0x1p100f, 1.f), fminf(r.y * 0x1p100f, 1.f)));
+          } else {                         // Σx₊⁴, Σx₊³, Σx₊²
+            const float2 r2 = fmul2(r, r);
+            A0 = ffma2(r2, r2, A0);
+            A1 = ffma2(r2, r, A1);
+            A2 = fadd2(A2, r2);
+          }
+        }
+        if constexpr (E == 1) {
+          a0 = (A0.x + A0.y) * 0.5f;
+          a1 = A1.x + A1.y;
+        } else if constexpr (E == 2) {
+          a0 = (A0.x + A0.y) * 0.25f;
+          a1 = (A1.x + A1.y) * 0.5f;
+          a2 = A2.x + A2.y;
+        } else {
+          a0 = (A0.x + A0.y) * 0.0625f;
+          a1 = (A1.x + A1.y) * 0.125f;
+          a2 = (A2.x + A2.y) * 0.25f;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) accum_f<E>(z[i] - rs.tau, ap, a0, a1, a2);
+      }
       block_sum3<NT>(a0, a1, a2, red, ph);
       solver_step(rs, a0, a1, a2, ap, halley);
     }
@@ -231,11 +276,23 @@ __global__ void __launch_bounds__(NT) fwd_reg_kernel(const T* s, int n, long lon
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     float v[W];
+    if constexpr (E == 2) {   // p = x₊² = (r/2)², r = x + |x|: packed, exact
+      const float2 nt = make_float2(-rs.tau, -rs.tau);
 #pragma unroll
-    for (int e = 0; e < W; ++e) {
-      float pu, uu;
-      p_and_u<E>(z[c * W + e] - rs.tau, ap, pu, uu);
-      v[e] = pu;
+      for (int e = 0; e < W; e += 2) {
+        const float2 x = fadd2(make_float2(z[c * W + e], z[c * W + e + 1]), nt);
+        const float2 h = fmul2(fadd2(x, fabs2(x)), make_float2(0.5f, 0.5f));
+        const float2 pp = fmul2(h, h);
+        v[e] = pp.x;
+        v[e + 1] = pp.y;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        float pu, uu;
+        p_and_u<E>(z[c * W + e] - rs.tau, ap, pu, uu);
+        v[e] = pu;
+      }
     }
     store_chunk<T>(prow, (c * NT + threadIdx.x) * W, n, v);
   }
