@@ -5,6 +5,7 @@ import torch
 import paper_2502_12082_b200 as P
 from tests.parity import make_case
 for (B, H, N, d, dt, causal) in [(1, 2, 300, 64, torch.bfloat16, True), (1, 1, 384, 128, torch.bfloat16, False),
+                                 (1, 2, 300, 128, torch.bfloat16, True),
                                  (1, 1, 200, 64, torch.float32, True)]:
     dev, _ = make_case(B, H, N, d, dt, seed=3)
     q, k, v, do = dev
