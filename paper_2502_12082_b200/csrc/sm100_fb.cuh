@@ -226,7 +226,9 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   __shared__ __align__(8) uint64_t bar_q, kv_full[NST], kv_empty[NST], s_full[NSB], p_full[NSB], o_full;
   __shared__ uint32_t tmem_base_sh;
 
-  const int i = blockIdx.x, bh = blockIdx.y;
+  // causal: the longest query blocks first (the block scheduler issues low indices first)
+  const int i = g.causal ? g.Tr - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long li = (long long)bh * g.Tr + i;
@@ -474,7 +476,9 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_first;                       // first tile (list order) with a non-zero dS in this CTA
 
-  const int i = blockIdx.x, bh = blockIdx.y;
+  // causal: the longest query blocks first (the block scheduler issues low indices first)
+  const int i = g.causal ? g.Tr - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long li = (long long)bh * g.Tr + i;

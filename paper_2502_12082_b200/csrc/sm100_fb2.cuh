@@ -52,7 +52,10 @@ out2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_ucnt;
 
-  const int i = blockIdx.x, bh = blockIdx.y;
+  // causal: the longest query blocks first (the block scheduler issues low indices first); pairs stay
+  // (even = cluster rank 0, odd)
+  const int i = g.causal ? (((int)gridDim.x - 2 - ((int)blockIdx.x & ~1)) | ((int)blockIdx.x & 1)) : (int)blockIdx.x;
+  const int bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();

@@ -143,7 +143,9 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
   __shared__ uint32_t tmem_base_sh;
   __shared__ int s_fallback, s_overflow;
 
-  const int i = blockIdx.x, bh = blockIdx.y;
+  // causal: the longest query blocks first (the block scheduler issues low indices first)
+  const int i = g.causal ? g.Tr - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int bh = blockIdx.y;
   const int b = bh / g.H, h = bh - b * g.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkb = g.visible_kblocks(i);
