@@ -5,7 +5,6 @@
 #include "sm100_tau.cuh"
 #include "sm100_fb.cuh"
 #include "sm100_fb2.cuh"
-#include "sm100_dkdv64.cuh"
 #include "tmap.h"
 
 namespace entmax {
@@ -31,12 +30,6 @@ constexpr size_t dq_smem() {
 constexpr int kOutMW = ENTMAX_OUT_MW;
 #ifndef ENTMAX_DQ_MW
 #define ENTMAX_DQ_MW 8      // math warps of the dQ kernel (16 measured slower: 1.075 -> 1.133 ms at config 2)
-#endif
-#ifndef ENTMAX_DKDV64
-#define ENTMAX_DKDV64 0      // d = 64: half-block units with double-buffered Sᵀ/dPᵀ (sm100_dkdv64.cuh): slower
-#endif
-#ifndef ENTMAX_DKDV64_MW
-#define ENTMAX_DKDV64_MW 16
 #endif
 #ifndef ENTMAX_DKDV_MW
 #define ENTMAX_DKDV_MW 16   // math warps of the dK/dV kernel (8: 1.64 ms, 16: 1.43 ms at config 2)
@@ -128,18 +121,6 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
           cudaStream_t st) {
   CUtensorMap tq, tk, tv, tdo;
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
-#if ENTMAX_DKDV64
-  if constexpr (D == 64) {
-    const size_t sm = dkdv_smem<D>();
-    constexpr int MW = ENTMAX_DKDV64_MW;
-    if (int rc = set_smem(dkdv64_kernel<E, CU, MW>, sm)) return rc;
-    ProfScope ps("dkdv_sm100", st);
-    if (cudaError_t e = launch_pdl(dkdv64_kernel<E, CU, MW>, dim3(g.Tc, g.B * g.H), dim3(dkdv_threads<MW>()), sm, st,
-                                   tq, tk, tv, tdo, g, ap, td, col_cnt, col_idx, kbar, (__nv_bfloat16*)dk,
-                                   (__nv_bfloat16*)dv))
-      return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
-  } else
-#endif
   {
     const size_t sm = dkdv_smem<D>();
     constexpr int MW = ENTMAX_DKDV_MW;
