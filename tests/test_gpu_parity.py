@@ -297,3 +297,20 @@ def test_parity_near_duplicate_keys(N, causal, d):
     for bh in range(2):
         out = check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
         assert out["dQ"] <= 1e-2, out
+
+
+@pytest.mark.parametrize("N,causal,rho", [(1152, False, 0.25), (1152, True, 0.25), (1408, True, 0.25)])
+def test_parity_pair_output_pass_d128(N, causal, rho):
+    """d = 128 runs the output pass on CTA pairs with 2-SM MMAs (sm100_fb2.cuh): the two query blocks of
+    a pair visit the union of their candidate lists.  Planted block sparsity gives adjacent query blocks
+    different lists (a block in one list only must contribute exact zeros to the other CTA's rows, and
+    each CTA's mask / 𝒬 table must stay its own), and an odd T_r leaves the last pair with a CTA past
+    the end; O, O⁽²⁾, τ, the mask, the tables and the gradients are checked against the oracle."""
+    _require_gpu()
+    spec = synth.HeadSpec("planted", rho=rho)
+    dev, ref = make_case(1, 2, N, 128, torch.bfloat16, seed=int(N * 10 + 100 * rho) + causal, spec=spec)
+    fw, grads = run_gpu(dev, 1.5, causal, 3)
+    half = fw.mask.shape[2] // 2   # the two query blocks of some pair must have different block sets
+    assert bool((fw.mask[:, :, 0:2 * half:2] != fw.mask[:, :, 1:2 * half:2]).any())
+    for bh in range(2):
+        check_head(fw, ref, bh, 1.5, causal, 3, torch.bfloat16, grads=grads)
