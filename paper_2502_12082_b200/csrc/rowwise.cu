@@ -14,7 +14,9 @@
 // memory (L2) on every pass.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <type_traits>
 
 #include "entmax_rowwise.h"
@@ -160,15 +162,25 @@ __device__ __forceinline__ float u_of_p(float p, const AlphaParams& ap) {
   return p > 0.f ? exp2f((2.0f - ap.alpha) * __log2f(p)) : 0.f;
 }
 
+// L2 prefetch of the row a later CTA will solve (1-D bulk prefetch, one instruction for the whole row;
+// `bytes` a multiple of 16).  The register kernels issue their row's loads only when the CTA starts,
+// so HBM traffic in flight is bounded by the resident CTAs; a CTA starting on a row that is already in
+// L2 finishes sooner.
+__device__ __forceinline__ void prefetch_row_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // ------------------------------------------------------------------------- register-resident rows
 template <typename T, int NT, int VPT, int E>
 __global__ void __launch_bounds__(NT) fwd_reg_kernel(const T* s, int n, long long ld, AlphaParams ap,
                                                      int n_iter, int halley, bool compact, T* p,
-                                                     float* __restrict__ tau) {
+                                                     float* __restrict__ tau, int pf) {
   constexpr int W = Chunk<T>::W, NC = VPT / W;
   __shared__ float red[2 * 3 * (NT / 32)];
   int ph = 0;
   const long long row = blockIdx.x;
+  if (pf && threadIdx.x == 0 && row + pf < gridDim.x)
+    prefetch_row_l2(s + (row + pf) * ld, ((uint32_t)n * (uint32_t)sizeof(T)) & ~15u);
   const T* srow = s + row * ld;
   float z[VPT];
   // Alg. 1 line 3: z = (α−1)·s; line 4: m = max z (padding entries past n: a huge finite negative value,
@@ -301,11 +313,13 @@ __global__ void __launch_bounds__(NT) fwd_reg_kernel(const T* s, int n, long lon
 
 template <typename T, int NT, int VPT, int E>
 __global__ void __launch_bounds__(NT) bwd_reg_kernel(const T* p, const T* dp, int n,
-                                                     long long ld, AlphaParams ap, T* ds) {
+                                                     long long ld, AlphaParams ap, T* ds, int pf) {
   constexpr int W = Chunk<T>::W, NC = VPT / W;
   __shared__ float red[2 * 3 * (NT / 32)];
   int ph = 0;
   const long long row = blockIdx.x;
+  if (pf && threadIdx.x < 2 && row + pf < gridDim.x)
+    prefetch_row_l2((threadIdx.x ? dp : p) + (row + pf) * ld, ((uint32_t)n * (uint32_t)sizeof(T)) & ~15u);
   float u[VPT], g[VPT];
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -417,6 +431,27 @@ __global__ void __launch_bounds__(kStreamNT) bwd_stream_kernel(const T* p, const
 }
 
 // ------------------------------------------------------------------------- dispatch
+// Prefetch distance of the register kernels: the resident CTAs of the whole GPU (the row the CTA that
+// replaces this one will solve), times ENTMAX_RW_PF (diagnostics; 0 disables).
+inline int pf_factor() {
+  static const int f = [] {
+    const char* e = std::getenv("ENTMAX_RW_PF");
+    return e ? std::atoi(e) : 1;
+  }();
+  return f;
+}
+template <auto Kern>
+int pf_distance(int nt, size_t smem) {
+  static int resident = -1;
+  if (resident < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, Kern, nt, smem) != cudaSuccess) per_sm = 1;
+    resident = std::max(1, per_sm) * sms;
+  }
+  return resident * pf_factor();
+}
 // Register-path shapes (NT threads × VPT values): chosen by n so a CTA holds its whole row.
 template <typename T, int E, typename Op>
 int by_n(int n, Op&& op) {
@@ -455,7 +490,8 @@ struct FwdLaunch {
       ProfScope ps("rowwise_fwd", st);
       const bool compact = n_iter > 4;
       fwd_reg_kernel<T, NT, VPT, E><<<(unsigned)rows, NT, compact ? smem : 0, st>>>(s, n, ld, ap, n_iter, halley,
-                                                                                  compact, p, tau);
+                                                                                  compact, p, tau,
+                                                                                  pf_distance<fwd_reg_kernel<T, NT, VPT, E>>(NT, compact ? smem : 0));
     }
     return cuda_status("entmax_rowwise_fwd");
   }
@@ -471,7 +507,8 @@ struct BwdLaunch {
       bwd_stream_kernel<T, E><<<(unsigned)rows, kStreamNT, 0, st>>>(p, dp, n, ld, ap, ds);
     } else {
       ProfScope ps("rowwise_bwd", st);
-      bwd_reg_kernel<T, NT, VPT, E><<<(unsigned)rows, NT, 0, st>>>(p, dp, n, ld, ap, ds);
+      bwd_reg_kernel<T, NT, VPT, E><<<(unsigned)rows, NT, 0, st>>>(p, dp, n, ld, ap, ds,
+                                                                pf_distance<bwd_reg_kernel<T, NT, VPT, E>>(NT, 0));
     }
     return cuda_status("entmax_rowwise_bwd");
   }
