@@ -68,8 +68,14 @@ const char* entmax_attn_status_string(int status);
 /* Detail message of the calling thread's last failing call ("" if none). */
 const char* entmax_attn_last_error(void);
 
-/* Mask / table granularity (B_r, B_c) used by every kernel of this library. */
-void entmax_attn_block_size(int32_t* Br, int32_t* Bc);
+/*
+ * Mask / table granularity (B_r, B_c) for head dim d and element type dtype (the block
+ * size the paper leaves open, P:L340-341 / reading c15).  Every supported (d, dtype) uses
+ * B_r = B_c = 128 in this build.  Br, Bc out (either may be NULL).  Returns ENTMAX_OK, or
+ * ENTMAX_ERR_INVALID_ARG for an unknown dtype, ENTMAX_ERR_UNSUPPORTED for a head dim no kernel
+ * handles (d not in {16, 32, 64, 128}); the outputs are then left untouched.
+ */
+int entmax_attn_block_size(int32_t d, int dtype, int32_t* Br, int32_t* Bc);
 
 /* Device workspace (bytes) needed by entmax_attn_fwd / entmax_attn_bwd for this shape. */
 size_t entmax_attn_fwd_workspace_bytes(const entmax_shape_t* shp, int dtype, int causal);

@@ -33,10 +33,11 @@ __all__ = ["entmax_attn_fwd", "entmax_attn_bwd", "entmax_attention", "block_size
 _DT = {torch.bfloat16: ENTMAX_BF16, torch.float32: ENTMAX_FP32}
 
 
-def block_size():
-    """(B_r, B_c): mask / lookup-table granularity of the library."""
+def block_size(d: int = 64, dtype=torch.bfloat16):
+    """(B_r, B_c): mask / lookup-table granularity of the library for head dim d and dtype."""
     br, bc = ctypes.c_int32(), ctypes.c_int32()
-    _lib.lib().entmax_attn_block_size(ctypes.byref(br), ctypes.byref(bc))
+    st = _lib.lib().entmax_attn_block_size(int(d), _DT[dtype], ctypes.byref(br), ctypes.byref(bc))
+    _lib.check(st, "entmax_attn_block_size")
     return br.value, bc.value
 
 
@@ -95,7 +96,7 @@ def _check_fwd_result(r: FwdResult, q: torch.Tensor, training: bool, masked: boo
     """Shapes, dtypes, layouts and device of a FwdResult against q (the kernels index τ by
     bh·N + row and the tables by B·H·T_r·T_c: a mismatch would read or write out of bounds)."""
     B, H, N, d = q.shape
-    br, bc = block_size()
+    br, bc = block_size(d, q.dtype)
     Tr, Tc = -(-N // br), -(-N // bc)
 
     def chk(t, shape, dtype, name, contiguous=True):
@@ -128,7 +129,7 @@ def entmax_attn_fwd(q, k, v, alpha=1.5, causal=False, n_iter=3, scale=None, trai
     L = _lib.lib()
     s = _shape(q)
     B, H, N, d = q.shape
-    br, bc = block_size()
+    br, bc = block_size(d, q.dtype)
     Tr, Tc = -(-N // br), -(-N // bc)
     dev = q.device
     if out is None:

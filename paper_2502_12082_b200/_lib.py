@@ -47,8 +47,9 @@ def lib() -> ctypes.CDLL:
     L.entmax_attn_status_string.argtypes = [i32]
     L.entmax_attn_last_error.restype = ctypes.c_char_p
     L.entmax_attn_last_error.argtypes = []
-    L.entmax_attn_block_size.restype = None
-    L.entmax_attn_block_size.argtypes = [ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+    L.entmax_attn_block_size.restype = ctypes.c_int
+    L.entmax_attn_block_size.argtypes = [ctypes.c_int32, ctypes.c_int, ctypes.POINTER(ctypes.c_int32),
+                                         ctypes.POINTER(ctypes.c_int32)]
     for fn in (L.entmax_attn_fwd_workspace_bytes, L.entmax_attn_bwd_workspace_bytes):
         fn.restype = sz
         fn.argtypes = [pshape, i32, i32]

@@ -191,9 +191,12 @@ const char* entmax_attn_status_string(int status) {
 
 const char* entmax_attn_last_error(void) { return g_last_error.c_str(); }
 
-void entmax_attn_block_size(int32_t* Br, int32_t* Bc) {
+int entmax_attn_block_size(int32_t d, int dtype, int32_t* Br, int32_t* Bc) {
+  if (dtype != ENTMAX_BF16 && dtype != ENTMAX_FP32) return fail(ENTMAX_ERR_INVALID_ARG, "unknown dtype %d", dtype);
+  if (d != 16 && d != 32 && d != 64 && d != 128) return fail(ENTMAX_ERR_UNSUPPORTED, "head dim %d not supported", d);
   if (Br) *Br = kBr;
   if (Bc) *Bc = kBc;
+  return ENTMAX_OK;
 }
 
 size_t entmax_attn_fwd_workspace_bytes(const entmax_shape_t* shp, int dtype, int causal) {

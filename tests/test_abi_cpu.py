@@ -41,8 +41,16 @@ def test_status_strings_and_block_size():
     assert L.entmax_attn_status_string(0) == b"ok"
     assert L.entmax_attn_status_string(3) == b"workspace too small"
     br, bc = ctypes.c_int32(), ctypes.c_int32()
-    L.entmax_attn_block_size(ctypes.byref(br), ctypes.byref(bc))
-    assert (br.value, bc.value) == (128, 128)
+    for d in (16, 32, 64, 128):
+        for dt in (0, 1):
+            br.value = bc.value = 0
+            assert L.entmax_attn_block_size(d, dt, ctypes.byref(br), ctypes.byref(bc)) == 0
+            assert (br.value, bc.value) == (128, 128)
+    br.value = bc.value = -1
+    assert L.entmax_attn_block_size(96, 0, ctypes.byref(br), ctypes.byref(bc)) == 2   # unsupported head dim
+    assert L.entmax_attn_block_size(64, 7, ctypes.byref(br), ctypes.byref(bc)) == 1   # unknown dtype
+    assert (br.value, bc.value) == (-1, -1)   # outputs untouched on error
+    assert L.entmax_attn_block_size(64, 0, None, None) == 0
 
 
 def test_workspace_sizes_scale_with_blocks():
