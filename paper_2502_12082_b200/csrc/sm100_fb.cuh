@@ -814,14 +814,24 @@ dkdv_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUte
     const int key = j * kBc + r;
     const bool valid = key < g.N;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    // per-tile addressing kept out of the loop body: shared addresses as 32-bit offsets, the stage index
+    // and phase as running counters; the 𝒦 list is read only for the causal diagonal test (the list is
+    // ascending from i0 = j, so only its first entry can be the diagonal block)
+    const uint32_t stage_a0 = ptx::smem_u32(sStage) + 2 * C::TILE + wg * (CW * 4);
+    const uint32_t qdf_a0 = ptx::smem_u32(qd_full), sfull_a = ptx::smem_u32(&s_full);
+    const bool diag0 = g.causal && cnt > 0 && list[0] == j;
+    int st = 0;
+    uint32_t qph = 0;
     for (int k = 0; k < cnt; ++k) {
-      const int ib = list[k], st = k % NST;
-      const uint8_t* stg = sStage + st * STAGE;
-      const uint32_t tq4 = ptx::smem_u32(stg + 2 * C::TILE) + wg * (CW * 4);   // τ_i (float4 units below)
-      const uint32_t dl4 = tq4 + 512;                                        // δ_i
-      const bool diag = g.causal && ib == j;   // queries below the key inside the diagonal block
-      ptx::mbar_wait(&qd_full[st], (k / NST) & 1);   // τ_i, δ_i staged by the producer warp
-      ptx::mbar_wait(&s_full, k & 1);
+      const uint32_t tq4 = stage_a0 + st * STAGE;   // τ_i (float4 units below)
+      const uint32_t dl4 = tq4 + 512;               // δ_i
+      const bool diag = diag0 && k == 0;            // queries below the key inside the diagonal block
+      ptx::mbar_wait_addr(qdf_a0 + 8 * st, qph);    // τ_i, δ_i staged by the producer warp
+      if (++st == NST) {
+        st = 0;
+        qph ^= 1u;
+      }
+      ptx::mbar_wait_addr(sfull_a, k & 1);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(2, 8 * k + 3);
       ptx::tc_fence_after();
       uint32_t pp[WPR], pd[WPR];

@@ -64,6 +64,10 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) ptx::mbar_arrive(bar);
 }
+__device__ __forceinline__ void warp_arrive_addr(uint32_t bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) ptx::mbar_arrive_addr(bar);
+}
 
 // compact per-block flags flags[0..n) into an increasing index list (one math warp)
 // A block list: the compacted table entries, or — in the unmasked mode (table == nullptr, SURVEY §8f

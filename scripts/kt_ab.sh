@@ -1,0 +1,7 @@
+# A/B per-kernel times: bash scripts/kt_ab.sh LIB_A LIB_B (paths relative to the repo root)
+for L in "$@"; do
+  echo LIB=$L
+  for a in "4 12 8192 64 1.5 0" "8 12 1024 64 1.5 1" "1 16 32768 128 1.5 1"; do
+    ENTMAX_ATTN_LIB=$PWD/$L python scripts/kernel_times.py $a
+  done
+done
