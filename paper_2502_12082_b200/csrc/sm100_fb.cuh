@@ -314,12 +314,17 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const int cta_last = g.causal ? i * kBr : g.N - 1;
     const float tr = valid ? tau[(long long)bh * g.N + row] : kPadTau;
     const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    // barrier addresses as 32-bit shared offsets and the buffer index / phase as running counters (no
+    // per-tile generic→shared conversion or division)
+    const uint32_t sfull_a0 = ptx::smem_u32(s_full), pfull_a0 = ptx::smem_u32(p_full);
+    int sb = 0;
+    uint32_t sph = 0;
     float usum = 0.f;
     for (int k = 0; k < ncand; ++k) {
-      const int j = list[k], sb = k % NSB;
+      const int j = list[k];
       const bool masked = (j + 1) * kBc - 1 > cta_last;
       const uint32_t col = lane_base + sb * 128 + wg * CW;
-      ptx::mbar_wait(&s_full[sb], (k / NSB) & 1);
+      ptx::mbar_wait_addr(sfull_a0 + 8 * sb, sph);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 3);
       ptx::tc_fence_after();
       float s0[32], s1[32];
@@ -385,9 +390,13 @@ out_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       }
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      warp_arrive(&p_full[sb]);
+      warp_arrive_addr(pfull_a0 + 8 * sb);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(1, 8 * k + 6);
       if (__any_sync(0xffffffffu, xmax > 0.f) && lane == 0) aflag[j] = 1;
+      if (++sb == NSB) {
+        sb = 0;
+        sph ^= 1u;
+      }
     }
     // epilogue: O and O⁽²⁾ = (Σ U V)/ΣU; each column half written by its warpgroup
     xch[tid] = usum;
@@ -573,11 +582,16 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
     const float dl = valid ? delta[(long long)bh * g.N + row] : 0.f;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     bool seen = false;   // this warp has seen a non-zero dS (the CTA's first such tile picks K̄, r12)
+    // barrier addresses as 32-bit shared offsets, dS buffer index / phase as running counters
+    const uint32_t sfull_a = ptx::smem_u32(&s_full), sempty_a = ptx::smem_u32(&s_empty);
+    const uint32_t dsf_a0 = ptx::smem_u32(ds_full), dse_a0 = ptx::smem_u32(ds_empty);
+    int db = 0;
+    uint32_t dph = 0;
     for (int k = 0; k < cnt; ++k) {
       const int jb = list[k];
       const bool masked = (jb + 1) * kBc - 1 > cta_last;
       const int key0 = jb * kBc + wg * CW;
-      ptx::mbar_wait(&s_full, k & 1);
+      ptx::mbar_wait_addr(sfull_a, k & 1);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 3);
       ptx::tc_fence_after();
       uint32_t pd[WPR];
@@ -592,7 +606,7 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
       }
       ptx::tmem_wait_ld();
       ptx::tc_fence_before();
-      warp_arrive(&s_empty);
+      warp_arrive_addr(sempty_a);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 4);
 #pragma unroll
       for (int hh = 0; hh < NH; ++hh) {
@@ -642,16 +656,19 @@ dq_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtens
         seen = __any_sync(0xffffffffu, (orv & 0x7fff7fffu) != 0u);
         if (seen && lane == 0) atomicMin(&s_first, k);
       }
-      const int db = k % NDS;
-      ptx::mbar_wait(&ds_empty[db], ((k / NDS) & 1) ^ 1);   // dQ(k−NDS) has consumed this dS buffer
+      ptx::mbar_wait_addr(dse_a0 + 8 * db, dph ^ 1u);   // dQ(k−NDS) has consumed this dS buffer
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 5);
       ptx::tc_fence_after();
       if constexpr (WPR == 32) ptx::tmem_st32(lane_base + t_ds + 64 * db + wg * WPR, pd);
       else ptx::tmem_st16(lane_base + t_ds + 64 * db + wg * WPR, pd);
       ptx::tmem_wait_st();
       ptx::tc_fence_before();
-      warp_arrive(&ds_full[db]);
+      warp_arrive_addr(dsf_a0 + 8 * db);
       if (threadIdx.x == 0) ENTMAX_TRACE_K(3, 8 * k + 6);
+      if (++db == NDS) {
+        db = 0;
+        dph ^= 1u;
+      }
     }
     float rho = 0.f;
     if (cnt > 0) {
