@@ -21,5 +21,9 @@ for N in (600, 1100):   # long rows (fp32 U) next to the short-row consistent-U 
 p, t = P.entmax_rowwise_fwd(torch.randn(8, 1000, device="cuda"), 1.5, 3)
 P.entmax_rowwise_bwd(p, torch.randn_like(p), 1.5)
 p, t = P.entmax_rowwise_fwd(torch.randn(4, 20000, device="cuda"), 1.5, 23, halley=False)
+# more rows than resident CTAs: every register-kernel CTA bulk-prefetches a later row into L2
+for dt in (torch.bfloat16, torch.float32):
+    p, t = P.entmax_rowwise_fwd(torch.randn(1500, 4096, device="cuda", dtype=dt), 1.5, 3)
+    P.entmax_rowwise_bwd(p, torch.randn_like(p), 1.5)
 torch.cuda.synchronize()
 print("sanitize case ok")
