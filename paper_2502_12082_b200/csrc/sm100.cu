@@ -5,7 +5,6 @@
 #include "sm100_tau.cuh"
 #include "sm100_fb.cuh"
 #include "sm100_fb2.cuh"
-#include "sm100_dkdv_slc.cuh"
 #include "tmap.h"
 
 namespace entmax {
@@ -34,9 +33,6 @@ constexpr int kOutMW = ENTMAX_OUT_MW;
 #endif
 #ifndef ENTMAX_DKDV_MW
 #define ENTMAX_DKDV_MW 16   // math warps of the dK/dV kernel (8: 1.64 ms, 16: 1.43 ms at config 2)
-#endif
-#ifndef ENTMAX_DKDV_SLC
-#define ENTMAX_DKDV_SLC 0   // d = 64: dK/dV with per-slice handshakes (sm100_dkdv_slc.cuh): slower, off
 #endif
 
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
@@ -125,15 +121,7 @@ int bwd_t(const void* q, const void* k, const void* v, const void* dO, const Geo
           cudaStream_t st) {
   CUtensorMap tq, tk, tv, tdo;
   if (int rc = tmaps(g, {{&tq, q}, {&tk, k}, {&tv, v}, {&tdo, dO}})) return rc;
-  if constexpr (D == 64 && ENTMAX_DKDV_SLC) {
-    const size_t sm = dkdv_smem<D>();
-    if (int rc = set_smem(dkdv_slc_kernel<E, CU>, sm)) return rc;
-    ProfScope ps("dkdv_sm100", st);
-    if (cudaError_t e = launch_pdl(dkdv_slc_kernel<E, CU>, dim3(g.Tc, g.B * g.H), dim3(dkdv_threads<kSlcMW>()), sm, st,
-                                   tq, tk, tv, tdo, g, ap, td, col_cnt, col_idx, kbar, (__nv_bfloat16*)dk,
-                                   (__nv_bfloat16*)dv))
-      return fail(ENTMAX_ERR_CUDA, "dkdv_sm100 launch: %s", cudaGetErrorString(e));
-  } else {
+  {
     const size_t sm = dkdv_smem<D>();
     constexpr int MW = ENTMAX_DKDV_MW;
     if (int rc = set_smem(dkdv_kernel<D, E, CU, MW>, sm)) return rc;
