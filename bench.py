@@ -194,6 +194,60 @@ def oracle_sample(cfg, seed=0, rows=512):
     return dt, flops, f"1 head x {rows} query rows of N={cfg['N']} d={cfg['d']} (fwd+bwd, float64 numpy)"
 
 
+def cpu_model():
+    """The host CPU model (BASELINE.md §3 asks for it next to the core count)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _pool_init():
+    try:
+        import threadpoolctl
+        threadpoolctl.threadpool_limits(1)
+    except Exception:
+        pass
+
+
+def _pool_rows(args):
+    cfg, seed, r0, r1 = args
+    import oracle as O
+    import synth
+    import torch
+    spec = synth.HeadSpec(cfg["gen"], rho=cfg.get("rho", 1.0))
+    q, k, v, do = spec.head(cfg["N"], cfg["d"], seed, 0, 0)
+    q, k, v, do = [torch.from_numpy(x).to(torch.bfloat16).double().numpy() for x in (q, k, v, do)]
+    rsel = np.arange(r0, r1)
+    fw = O.attn_fwd(q, k, v, cfg["alpha"], cfg["causal"], cfg["n_iter"], rows=rsel)
+    tau_all = np.zeros(cfg["N"])
+    tau_all[rsel] = fw["tau"]
+    O.attn_bwd(q, k, v, do, tau_all, cfg["alpha"], cfg["causal"], rows=rsel)
+    return len(rsel)
+
+
+def oracle_sample_pool(cfg, rows_per_worker=64, seed=0):
+    """BASELINE.md §3 timing mode (ii): a process pool, one worker per host core with one BLAS thread each,
+    unit = a chunk of query rows of one head (fwd + bwd).  Returns (seconds, effective flops, workers)."""
+    import multiprocessing as mp
+    workers = len(os.sched_getaffinity(0))
+    rows = min(rows_per_worker * workers, cfg["N"])
+    chunks = [(dict(cfg), seed, r, min(r + rows_per_worker, rows)) for r in range(0, rows, rows_per_worker)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers, initializer=_pool_init) as pool:
+        pool.map(_pool_rows, chunks[:workers])          # warm-up (imports, first-touch)
+        t0 = time.perf_counter()
+        pool.map(_pool_rows, chunks)
+        dt = time.perf_counter() - t0
+    pairs = sum(min(r + 1, cfg["N"]) if cfg["causal"] else cfg["N"] for r in range(rows))
+    return dt, 14.0 * cfg["d"] * pairs, workers
+
+
 def cpu_cores():
     try:
         import threadpoolctl
@@ -223,7 +277,8 @@ def run_reference(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample": desc},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                         "cpu_model": cpu_model(), "affinity_cores": len(os.sched_getaffinity(0))},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -588,7 +643,15 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, fl, desc = oracle_sample(dict(cfg), seed=0, rows=4096)
         line["cpu_baseline"] = {"value": fl / dt / 1e12, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
-                                "sample": desc, "seconds": dt}
+                                "sample": desc, "seconds": dt, "cpu_model": cpu_model(),
+                                "affinity_cores": len(os.sched_getaffinity(0))}
+        try:
+            pdt, pfl, pw = oracle_sample_pool(dict(cfg))
+            line["cpu_baseline"]["pool"] = {
+                "value": pfl / pdt / 1e12, "unit": UNIT, "workers": pw, "seconds": pdt,
+                "sample": f"{pw} processes x 64 query rows of one head (fwd+bwd, float64 numpy, 1 BLAS thread each)"}
+        except Exception as e:   # the pool leg is a reported extra, never a reason to fail the bench
+            line["cpu_baseline"]["pool"] = {"unavailable": str(e)[:200]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -28,3 +28,15 @@ def test_visible_pairs_matches_brute_force():
         full = np.ones_like(m)
         assert bench.visible_pairs_in_active_blocks(torch.from_numpy(full), N, causal, Br, Bc) == \
             3 * bench.total_visible_pairs(N, causal)
+
+
+def test_oracle_pool_timing_mode_and_cpu_model():
+    """BASELINE.md §3 mode (ii): the process-pool oracle leg runs one worker per host core and counts the
+    same effective flops as the single-process leg for the same rows."""
+    import os
+    cfg = dict(B=1, H=1, N=256, d=64, alpha=1.5, causal=True, n_iter=3, gen="gaussian")
+    dt, fl, workers = bench.oracle_sample_pool(cfg, rows_per_worker=4)
+    assert workers == len(os.sched_getaffinity(0)) and dt > 0
+    rows = min(4 * workers, 256)
+    assert fl == 14.0 * 64 * sum(min(r + 1, 256) for r in range(rows))
+    assert isinstance(bench.cpu_model(), str) and bench.cpu_model()
