@@ -231,7 +231,7 @@ def _pool_rows(args):
     return len(rsel)
 
 
-def oracle_sample_pool(cfg, rows_per_worker=64, seed=0):
+def oracle_sample_pool(cfg, rows_per_worker=512, seed=0):
     """BASELINE.md §3 timing mode (ii): a process pool, one worker per host core with one BLAS thread each,
     unit = a chunk of query rows of one head (fwd + bwd).  Returns (seconds, effective flops, workers)."""
     import multiprocessing as mp
@@ -649,7 +649,7 @@ def main():
             pdt, pfl, pw = oracle_sample_pool(dict(cfg))
             line["cpu_baseline"]["pool"] = {
                 "value": pfl / pdt / 1e12, "unit": UNIT, "workers": pw, "seconds": pdt,
-                "sample": f"{pw} processes x 64 query rows of one head (fwd+bwd, float64 numpy, 1 BLAS thread each)"}
+                "sample": f"{pw} processes x 512 query rows of one head (fwd+bwd, float64 numpy, 1 BLAS thread each)"}
         except Exception as e:   # the pool leg is a reported extra, never a reason to fail the bench
             line["cpu_baseline"]["pool"] = {"unavailable": str(e)[:200]}
     if rank == 0:
