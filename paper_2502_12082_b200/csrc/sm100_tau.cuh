@@ -78,6 +78,36 @@ __device__ __forceinline__ void accum_fx32(float x, const AlphaParams& ap, uint3
   p1 += fx23(t1);
   p2 += fx23(t2);
 }
+// accum_fx32<E> on a pair of x in packed f32x2 (E = 1, 2, 4), RAW: every term adds bits(t + 1) — the caller
+// subtracts 0x3f800000 per term (mod 2³²) once at the end.  r = x + |x| = 2x₊ exactly, and the powers of r
+// are scaled back by exact powers of two inside the fma that forms t + 1, so the terms are bitwise those
+// of accum_fx32 (where a power-of-two scaling would round differently — subnormal x₊² — every term is 0
+// anyway); [x > 0] = min(r · 2¹⁰⁰, 1) (r ≥ 2⁻⁵⁰ whenever x > 0).  x must be finite (pads: −1e30).
+template <int E>
+__device__ __forceinline__ void accum_fx32_pair_raw(float2 x, uint32_t& p0, uint32_t& p1, uint32_t& p2) {
+  const float2 one2 = make_float2(1.0f, 1.0f);
+  const float2 r = fadd2(x, fabs2(x));
+  auto bits2 = [](float2 v) { return __float_as_uint(v.x) + __float_as_uint(v.y); };
+  auto ind1 = [&]() {   // [x > 0] + 1
+    const float2 g = fmul2(r, make_float2(0x1p100f, 0x1p100f));
+    return fadd2(make_float2(fminf(g.x, 1.0f), fminf(g.y, 1.0f)), one2);
+  };
+  if constexpr (E == 4) {
+    const float2 r2 = fmul2(r, r);
+    p0 += bits2(ffma2(fmul2(r2, r2), make_float2(0.0625f, 0.0625f), one2));
+    p1 += bits2(ffma2(fmul2(r2, r), make_float2(0.125f, 0.125f), one2));
+    p2 += bits2(ffma2(r2, make_float2(0.25f, 0.25f), one2));
+  } else if constexpr (E == 2) {
+    p0 += bits2(ffma2(fmul2(r, r), make_float2(0.25f, 0.25f), one2));
+    p1 += bits2(ffma2(r, make_float2(0.5f, 0.5f), one2));
+    p2 += bits2(ind1());
+  } else {   // E == 1: x₊, [x > 0], 0
+    p0 += bits2(ffma2(r, make_float2(0.5f, 0.5f), one2));
+    p1 += bits2(ind1());
+    p2 += 2u * 0x3f800000u;   // t = 0 (kept in the raw convention)
+  }
+}
+
 template <int E>
 __device__ __forceinline__ void accum_fx(float x, const AlphaParams& ap, float u2, FxSum& q) {
   if constexpr (E != 0) {
@@ -468,16 +498,29 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
       constexpr int kReg = 12;
       float lr[kReg];
 #pragma unroll
-      for (int c = 0; c < kReg; ++c) lr[c] = c < n ? ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u) : -INFINITY;
+      // (finite pads: the packed sums below form x + |x|)
+      for (int c = 0; c < kReg; ++c) lr[c] = c < n ? ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u) : -1e30f;
       for (int t = 0; t < n_iter; ++t) {
         float a0, a1, a2;
         if constexpr (E != 0) {   // <= 4·kCapQ (< 256) terms per row: 32-bit fixed-point sums
+          // pairs of entries in packed f32x2 (accum_fx32_pair_raw: bitwise the terms of accum_fx32)
           uint32_t p0 = 0, p1 = 0, p2 = 0;
+          const float2 cp2 = make_float2(ap.cp, ap.cp), nt2 = make_float2(-rq.tau, -rq.tau);
 #pragma unroll
-          for (int c = 0; c < kReg; ++c) accum_fx32<E>(fmaf(lr[c], ap.cp, -rq.tau), ap, p0, p1, p2);
-#pragma unroll 4
-          for (int c = kReg; c < n; ++c)
-            accum_fx32<E>(fmaf(ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u), ap.cp, -rq.tau), ap, p0, p1, p2);
+          for (int c = 0; c < kReg; c += 2)
+            accum_fx32_pair_raw<E>(ffma2(make_float2(lr[c], lr[c + 1]), cp2, nt2), p0, p1, p2);
+          int nterms = kReg;
+#pragma unroll 2
+          for (int c = kReg; c < n; c += 2) {
+            const float v0 = ptx::ld_shared_f32(ls0r + (uint32_t)c * 512u);
+            const float v1 = c + 1 < n ? ptx::ld_shared_f32(ls0r + (uint32_t)(c + 1) * 512u) : -1e30f;
+            accum_fx32_pair_raw<E>(ffma2(make_float2(v0, v1), cp2, nt2), p0, p1, p2);
+            nterms += 2;
+          }
+          const uint32_t bias = (uint32_t)nterms * 0x3f800000u;
+          p0 -= bias;
+          p1 -= bias;
+          p2 -= bias;
 #pragma unroll
           for (int o = 1; o <= 2; o <<= 1) {
             p0 += __shfl_xor_sync(0xffffffffu, p0, o);
