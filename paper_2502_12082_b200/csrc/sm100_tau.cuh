@@ -604,36 +604,15 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 #pragma unroll
             for (int e = 1; e < 31; e += 2) cm = fmax3(cm, s[e], s[e + 1]);
             if (__any_sync(0xffffffffu, fmaf(cm, ap.cp, -rs.tau) > 0.f)) {
-              if constexpr (E == 4) {
-                // accum_fx32<4> on pairs in packed f32x2 (FFMA2/FADD2/FMUL2): r = x + |x| = 2x₊ exactly, so
-                // r², r²·r, (r²)² are 4x₊², 8x₊³, 16x₊⁴ with the same roundings as x₊², x₊³, x₊⁴ (power-of-two
-                // scalings commute with rounding; where they would not — subnormal x₊² — every fixed-point
-                // term is 0 anyway) and fma(·, 2^-k, 1) is the exact t + 1 of fx23: bitwise the same sums
+              if constexpr (E != 0) {   // 32 terms per chunk on pairs in packed f32x2 (accum_fx32_pair_raw)
                 uint32_t p0 = 0, p1 = 0, p2 = 0;
                 const float2 cp2 = make_float2(ap.cp, ap.cp), nt2 = make_float2(-rs.tau, -rs.tau);
-                const float2 one2 = make_float2(1.0f, 1.0f);
 #pragma unroll
-                for (int e = 0; e < 32; e += 2) {
-                  const float2 x = ffma2(make_float2(s[e], s[e + 1]), cp2, nt2);
-                  const float2 r = fadd2(x, fabs2(x));
-                  const float2 r2 = fmul2(r, r);
-                  const float2 a = ffma2(fmul2(r2, r2), make_float2(0.0625f, 0.0625f), one2);
-                  const float2 b = ffma2(fmul2(r2, r), make_float2(0.125f, 0.125f), one2);
-                  const float2 c = ffma2(r2, make_float2(0.25f, 0.25f), one2);
-                  p0 += __float_as_uint(a.x) + __float_as_uint(a.y);
-                  p1 += __float_as_uint(b.x) + __float_as_uint(b.y);
-                  p2 += __float_as_uint(c.x) + __float_as_uint(c.y);
-                }
-                q.q0 += p0 - 32u * 0x3f800000u;   // (mod 2³²: the partials of 32 terms fit)
+                for (int e = 0; e < 32; e += 2)
+                  accum_fx32_pair_raw<E>(ffma2(make_float2(s[e], s[e + 1]), cp2, nt2), p0, p1, p2);
+                q.q0 += p0 - 32u * 0x3f800000u;   // (mod 2³²: 32 terms of at most 2²³ each)
                 q.q1 += p1 - 32u * 0x3f800000u;
                 q.q2 += p2 - 32u * 0x3f800000u;
-              } else if constexpr (E != 0) {   // 32 terms per chunk: 32-bit partials, widened once
-                uint32_t p0 = 0, p1 = 0, p2 = 0;
-#pragma unroll
-                for (int e = 0; e < 32; ++e) accum_fx32<E>(fmaf(s[e], ap.cp, -rs.tau), ap, p0, p1, p2);
-                q.q0 += p0;
-                q.q1 += p1;
-                q.q2 += p2;
               } else {
 #pragma unroll
                 for (int e = 0; e < 32; ++e) {
