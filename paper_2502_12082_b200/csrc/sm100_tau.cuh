@@ -366,10 +366,10 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
     const uint32_t cflag_s = ptx::smem_u32(cflag);
     const float inv_cp = 1.0f / ap.cp;    // (the 3e-6 margin dwarfs the product's rounding)
     // conservative score threshold: s <= thr(m) ⇒ fma(s, c', −τ_lo(m)) <= 0 (margin >> fma rounding)
-    auto thr_of = [&](float m) {
-      const float lo = m * ap.cp - 1.0f;
-      return valid ? (lo - fmaxf(fabsf(lo), 1e-6f) * 3.0e-6f) * inv_cp : INFINITY;
-    };
+    // = m − (1 + margin)/c′ with margin 3e-6·(|m|·c′ + 1.000001) >= the former max(|m·c′ − 1|, 1e-6)·3e-6: two
+    // instructions per refresh (FFMA with |m|, FADD), and never above the former threshold
+    const float thr_c = inv_cp * (1.0f + 3.0e-6f * 1.000001f);
+    auto thr_of = [&](float m) { return valid ? fmaf(fabsf(m), -3.0e-6f, m) - thr_c : INFINITY; };
 
     // One streaming pass appending the scores above the threshold to the thread's private list.
     // online: the threshold follows the running max of the row (own quarter + the row's published
@@ -395,8 +395,8 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
             const float* sg = s + 8 * gq;
             gm[gq] = fmax3(fmax3(sg[0], sg[1], sg[2]), fmax3(sg[3], sg[4], sg[5]), fmaxf(sg[6], sg[7]));
           }
+          const float tmax = fmax3(fmaxf(gm[0], gm[1]), gm[2], gm[3]);
           if (online && t < nkb) {
-            const float tmax = fmax3(fmaxf(gm[0], gm[1]), gm[2], gm[3]);
             if (tmax > mread) ptx::st_shared_f32(msh, fmaxf(tmax, mrun));
             mrun = fmax3(mrun, tmax, mread);
             thr = thr_of(mrun);                 // branch-free (same value when mrun is unchanged)
@@ -408,7 +408,7 @@ tau_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUten
 #ifdef ENTMAX_TAU_NOAPPEND
           if (thr != -12345.f) continue;   // diagnostics: timing of the common path only
 #endif
-          if (!__any_sync(0xffffffffu, (hit[0] | hit[1]) | (hit[2] | hit[3]))) continue;
+          if (!__any_sync(0xffffffffu, tmax > thr)) continue;   // (= any hit)
           if (lane == 0) ptx::st_shared_u8(cflag_s + j, 1);   // τ_lo candidate block (a superset when online)
           const uint32_t tag = (uint32_t)j;
           // groups of 8 keys with a candidate in some lane: warp-uniform branch.  A lane with one hit
